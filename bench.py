@@ -1,0 +1,381 @@
+"""Benchmark: QAOA objective evaluations/s for LABS (n=26, p=10, complex128) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n N] [--p P]
+
+One "step" = one full QAOA objective evaluation: |+>^n -> p x (phase, X mixer)
+-> sum_k c_k |psi_k|^2 (BASELINE.json north star, LABS n=26 p=10 fp64).
+
+* ``value``: device-resident throughput (cost diagonal resident in HBM, the
+  fused program enqueued back to back, CUDA events on the launching stream).
+  The 1 GiB state is ~8x the 126 MB L2, so no L2 flush is needed between steps.
+* ``e2e``: the same metric through the public API a user calls —
+  ``sim.simulate_qaoa(gammas, betas)`` + ``sim.get_expectation(result)`` —
+  angles from host memory each step (fresh values), the scalar read back.
+* ``roofline``: HBM bound of the dominant kernel (k_tile_pass); achieved =
+  algorithmic bytes of the step's tile passes / their time.
+* ``cpu_baseline``: the CPU oracle port (oracle/, C + OpenMP restatement of the
+  reference's numba kernels) on this host, bounded sample.
+* N > 1 (torchrun): the state is sharded by global qubits, weak scaling with
+  n = 26 + log2 N (2^26 amplitudes per GPU); exchanges are NCCL all-to-all.
+  ``value`` counts n=26-equivalent evaluations (one n-qubit evaluation =
+  2^(n-26) of them) so ideal weak scaling is N x the 1-GPU value.
+* ``--impl reference``: the reference algorithm's CPU implementation (the
+  oracle port; the reference is Python/numba, there is nothing to compile)
+  on all host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASE_N = 26
+METRIC = "QAOA objective evals/sec (LABS/MaxCut n=26–34); achieved HBM GB/s vs peak"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def angles(p, seed=0):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(0, 1, p), rng.uniform(0, 1, p)
+
+
+class ClockSampler:
+    """Samples SM clocks + throttle reasons via NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+        return False
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        reasons = [name for bit, name in self.REASONS.items() if self.reasons & bit and bit != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------- CPU (oracle port)
+def cpu_eval_rate(costs, p, g, b, layers_sample):
+    """Time `layers_sample` QAOA layers + one expectation with the oracle
+    (C + OpenMP), extrapolate to a p-layer evaluation."""
+    from oracle import oracle as O
+
+    n = costs.size.bit_length() - 1
+    st = O.uniform_state(n)
+    t0 = time.perf_counter()
+    for li in range(layers_sample):
+        O.apply_phase(st, costs, float(g[li % p]))
+        O.rx_layer(st, float(b[li % p]))
+    t_layers = (time.perf_counter() - t0) / layers_sample
+    t0 = time.perf_counter()
+    O.expectation_fast(st, costs)
+    t_exp = time.perf_counter() - t0
+    t_eval = p * t_layers + t_exp
+    return 1.0 / t_eval, t_layers, t_exp
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    n = args.n or BASE_N
+    p = args.p
+    g, b = angles(p)
+    threads = O.num_threads()
+    t0 = time.perf_counter()
+    costs = O.precompute_cost_vector(n, O.labs_terms(n))
+    t_pre = time.perf_counter() - t0
+    st = O.uniform_state(n)
+    # one step = one QAOA layer (phase + X mixer over all n qubits) of the
+    # p-layer evaluation; the objective rate combines p layers + 1 expectation.
+    for w in range(args.warmup):
+        O.apply_phase(st, costs, float(g[w % p]))
+        O.rx_layer(st, float(b[w % p]))
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        O.apply_phase(st, costs, float(g[s % p]))
+        O.rx_layer(st, float(b[s % p]))
+    t_layer = (time.perf_counter() - t0) / args.steps
+    t0 = time.perf_counter()
+    O.expectation_fast(st, costs)
+    t_exp = time.perf_counter() - t0
+    value = 1.0 / (p * t_layer + t_exp)
+    sample = (f"{args.steps} timed layers (phase + X mixer) of LABS n={n}; evals/s = 1/(p*t_layer + t_expectation), "
+              f"p={p}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_layer, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"LABS n={n} p={p} X-mixer complex128 objective evaluation", "n": n, "p": p,
+                   "step": "one QAOA layer", "l2": "state > L2"},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "precompute_s": t_pre, "ms_per_layer": 1e3 * t_layer, "ms_expectation": 1e3 * t_exp,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=0, help="total qubits (default 26 + log2 N)")
+    ap.add_argument("--p", type=int, default=10)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2309_04841_b200 import QaoaSimulator, _lib, labs_terms
+    from paper_2309_04841_b200.distributed import ShardedQaoaSimulator
+    from paper_2309_04841_b200.mixers import run_program
+
+    k = int(math.log2(world))
+    n = args.n or (BASE_N + k)
+    p = args.p
+    g, b = angles(p)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ------------------------------------------------------------ setup (+ precompute, timed separately)
+    barrier()
+    t0 = time.perf_counter()
+    poly = labs_terms(n)
+    if world == 1:
+        sim = QaoaSimulator(terms=poly)
+        dc = sim.device_costs
+    else:
+        sim = ShardedQaoaSimulator(poly)
+        dc = sim.costs
+    barrier()
+    precompute_s = time.perf_counter() - t0
+    n_local = n - k
+    S = 16 * (1 << n_local)
+    Cb = dc.nbytes_per_amp() * (1 << n_local)
+
+    # ------------------------------------------------------------ device-resident step
+    layers = [(float(gi), float(bi), 1, 0, n_local) for gi, bi in zip(g, b)]
+    if world == 1:
+        state = torch.empty(1 << n, dtype=torch.complex128, device="cuda")
+        exp_dev = torch.empty(1, dtype=torch.float64, device="cuda")
+        amp = 1.0 / math.sqrt(float(1 << n))
+
+        def step():
+            run_program(state, n, "x", layers, dc=dc, init=True, init_amp=amp, expectation_out=exp_dev)
+    else:
+        def step():
+            sim.simulate_qaoa(g, b, expectation=False)
+            loc = sim.ops.expectation(sim.shard, sim.costs)
+            dist.all_reduce(loc)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    units_per_eval = 2.0 ** (n - BASE_N) if world > 1 else 1.0
+    value = args.steps * units_per_eval / (ms / 1e3)
+
+    # ------------------------------------------------------------ byte model of the step (per GPU)
+    lay = (_lib.FqLayer * p)(*[_lib.FqLayer(*lt) for lt in layers])
+    passes = _lib.load().fq_plan_x_passes(n_local, p, lay)
+    n_phase = sum(1 for gi in g if gi != 0.0)
+    if world == 1:
+        tile_bytes = passes * 2 * S - S + (n_phase + 1) * Cb  # first pass generates |+>, last reads costs for E
+        launches = passes + 1
+    else:
+        post = p * (1 if k > 0 else 0)  # the k-position pass after each exchange
+        local_passes = passes * p if False else None
+        per_layer = _lib.load().fq_plan_x_passes(n_local, 1, lay)
+        tile_bytes = p * per_layer * 2 * S - S + n_phase * Cb + post * 2 * S + S + Cb
+        launches = p * (per_layer + (1 if k > 0 else 0)) + 2
+        del local_passes
+    peak, peak_kind = load_peaks()
+    achieved = tile_bytes / (ms_step / 1e3) / 1e9
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                tj = json.load(f)
+            if tj.get("n") == n_local:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ------------------------------------------------------------ e2e through the public API
+    e2e = None
+    if world == 1:
+        rng = np.random.default_rng(1)
+        sets = [(g + 1e-3 * rng.standard_normal(p), b + 1e-3 * rng.standard_normal(p))
+                for _ in range(args.steps + args.warmup)]
+        for i in range(args.warmup):
+            sim.get_expectation(sim.simulate_qaoa(*sets[i]))
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t_wall = time.perf_counter()
+        f0.record(stream)
+        vals = []
+        for i in range(args.warmup, args.warmup + args.steps):
+            res = sim.simulate_qaoa(*sets[i])
+            vals.append(sim.get_expectation(res))
+            del res
+        f1.record(stream)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+        e2e_ms = max(f0.elapsed_time(f1), 1e3 * t_wall)
+        e2e = {"value": args.steps / (e2e_ms / 1e3), "unit": "evals/s", "h2d_bytes_per_step": 2 * p * 8,
+               "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / args.steps,
+               "api": "QaoaSimulator.simulate_qaoa + get_expectation"}
+    else:
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            sim.simulate_qaoa(g, b, expectation=True)
+        f1.record(stream)
+        barrier()
+        t = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+        e2e = {"value": args.steps * units_per_eval / (e2e_ms / 1e3), "unit": "evals/s",
+               "h2d_bytes_per_step": 2 * p * 8, "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / args.steps,
+               "api": "ShardedQaoaSimulator.simulate_qaoa"}
+
+    # ------------------------------------------------------------ CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu:
+        from oracle import oracle as O
+
+        costs_host = sim.get_cost_diagonal()
+        layers_sample = 2
+        rate, t_layer, t_exp = cpu_eval_rate(np.array(costs_host), p, g, b, layers_sample)
+        cpu = {"value": rate, "unit": "evals/s", "cores": O.num_threads(), "kind": "port",
+               "sample": f"{layers_sample} of {p} layers (phase + X mixer) + 1 expectation of LABS n={n} on the "
+                         f"oracle C/OpenMP port, extrapolated to the p={p} evaluation "
+                         f"({1e3 * t_layer:.0f} ms/layer, {1e3 * t_exp:.0f} ms expectation)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": f"LABS n={n} p={p} X-mixer complex128 objective evaluation"
+                                   + (f" sharded over {world} GPUs (n_local={n_local}; value in n=26-equivalent "
+                                      f"evaluations)" if world > 1 else ""),
+                       "n": n, "p": p, "n_local": n_local, "angles": "default_rng(0) U(0,1)",
+                       "cost_encoding": "uint16 levels (lossless)" if dc.u16 is not None else "float64",
+                       "l2": "no flush: 1 GiB state per GPU >> 126 MB L2",
+                       "parallelism": f"state sharded over {world} GPUs" if world > 1 else "single GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "kernel": "k_tile_pass (all passes of the step)",
+                         "algorithmic_bytes_per_step": tile_bytes, "passes_per_step": passes if world == 1 else None},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches * args.steps,
+            "clocks": sampler.summary(),
+            "precompute_s": precompute_s,
+            "ms_per_layer": ms_step / p,
+            "objective": float(exp_dev.item()) if world == 1 else None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,190 @@
+/*
+ * fqaoa.h — C ABI of the B200-native QAOA hot path (libfqaoa.so, sm_100a).
+ *
+ * This is the drop-in seam for the reference's operator layer,
+ * fastqaoa/_kernels.py (the numba kernels every higher layer calls), plus
+ * fused entry points the per-qubit seam cannot express.
+ *
+ * Conventions (all functions):
+ *   - every pointer is a caller-owned DEVICE buffer unless noted "host";
+ *   - states are interleaved complex128 (re, im doubles), index bit q = qubit q
+ *     (reference statevec.py:3-4); cost vectors are float64 or uint16 levels;
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); work is
+ *     enqueued asynchronously and nothing here synchronises the host except
+ *     where stated;
+ *   - return 0 on success, otherwise an FQ_ERR_* code; fq_last_error() gives a
+ *     thread-local message.  No exception ever crosses the ABI;
+ *   - nothing allocates memory proportional to 2^n (in-place contract of
+ *     reference _kernels.py:1-6).  Reductions take `scratch`, a device buffer
+ *     of at least FQ_SCRATCH_DOUBLES doubles.
+ */
+#ifndef FQAOA_H
+#define FQAOA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FQ_OK 0
+#define FQ_ERR_ARG 1
+#define FQ_ERR_CUDA 2
+#define FQ_ERR_UNSUPPORTED 3
+
+#define FQ_SCRATCH_DOUBLES 4096
+
+/* mixer kinds (reference mixers.py:140-199, Mixer.KINDS) */
+#define FQ_MIXER_X 0
+#define FQ_MIXER_XY_RING 1
+#define FQ_MIXER_XY_COMPLETE 2
+#define FQ_MIXER_CUSTOM 3
+
+/* cost-vector encodings */
+#define FQ_COST_F64 0 /* double per amplitude (terms.py:102-120 output)       */
+#define FQ_COST_U16 1 /* uint16 level v, cost = scale*v + offset (terms.py:123-175) */
+
+int fq_version(void);
+const char *fq_last_error(void);
+/* Number of SMs of the current device (grid sizing), or -1. */
+int fq_sm_count(void);
+
+/* ------------------------------------------------------------------ *
+ * Operator layer — one entry per reference kernel.                     *
+ * ------------------------------------------------------------------ */
+
+/* replaces su2_on_pairs — reference _kernels.py:14-27 (callers mixers.py:71,84,91,
+ * distributed.py:147,152).  Pairs (l, l|2^q): y0 = a x0 - conj(b) x1,
+ * y1 = b x0 + conj(a) x1. */
+int fq_su2_on_pairs(void *psi, int64_t size, double a_re, double a_im, double b_re,
+                    double b_im, int q, void *stream);
+
+/* replaces xy_on_pairs — reference _kernels.py:30-48 (callers mixers.py:106,
+ * distributed.py:181,202).  Requires p_lo < p_hi. */
+int fq_xy_on_pairs(void *psi, int64_t size, double cos_b, double sin_b, int p_lo, int p_hi,
+                   void *stream);
+
+/* replaces swap_bits — reference _kernels.py:51-65 (callers distributed.py:194,207). */
+int fq_swap_bits(void *psi, int64_t size, int p_lo, int p_hi, void *stream);
+
+/* replaces phase_multiply — reference _kernels.py:68-73 (callers statevec.py:78,
+ * distributed.py:134).  psi[k] *= exp(-i gamma costs[k]). */
+int fq_phase_multiply(void *psi, const double *costs, int64_t size, double gamma, void *stream);
+
+/* replaces accumulate_terms — reference _kernels.py:76-94 (caller terms.py:118).
+ * out[k] += sum_t w_t (-1)^popcount((index_base+k) & masks[t]), accumulated per
+ * element left-to-right in term order exactly like the reference (bit-exact for
+ * any float weights).  index_base lets a shard evaluate its global slice. */
+int fq_accumulate_terms(double *out, int64_t size, const double *weights, const int64_t *masks,
+                        int64_t n_terms, int64_t index_base, void *stream);
+
+/* Exact-integer variant of fq_accumulate_terms for dyadic weights:
+ * w_t = iweights[t] * 2^-shift.  Accumulates in int64 and converts once, which
+ * equals the reference's sequential double sum bit-for-bit whenever
+ * sum_t |iweights[t]| < 2^53 (the host checks this before choosing it).
+ * acc_bits = 32 selects an int32 accumulator (valid when sum_t |iweights[t]| < 2^31),
+ * 64 an int64 one. */
+int fq_accumulate_terms_dyadic(double *out, int64_t size, const int64_t *iweights,
+                               const int64_t *masks, int64_t n_terms, int shift, int acc_bits,
+                               int64_t index_base, void *stream);
+
+/* Same exact-integer accumulation, emitted directly as uint16 levels
+ * v = (S(k) - level_offset) >> level_shift where S(k) = sum_t iweights[t]*sign.
+ * Used when the float64 diagonal does not fit (n=34, K=2).  *bad_dev (device
+ * int) is set nonzero if any value falls outside [0, 65535] or off the grid. */
+int fq_precompute_levels_u16(uint16_t *out, int64_t size, const int64_t *iweights,
+                             const int64_t *masks, int64_t n_terms, int acc_bits, int64_t index_base,
+                             int64_t level_offset, int level_shift, int *bad_dev, void *stream);
+
+/* replaces abs2_inplace — reference _kernels.py:97-102 (caller statevec.py:90). */
+int fq_abs2_inplace(void *psi, int64_t size, void *stream);
+
+/* ------------------------------------------------------------------ *
+ * States and observables (reference statevec.py)                      *
+ * ------------------------------------------------------------------ */
+
+/* uniform_state (statevec.py:22-29) when weight < 0, else
+ * hamming_weight_state (statevec.py:41-54) restricted to the slice
+ * [index_base, index_base+size).  amp = amplitude value of the support. */
+int fq_init_state(void *psi, int64_t size, int weight, double amp, int64_t index_base,
+                  void *stream);
+
+/* expectation (statevec.py:94-97): *out_dev = sum_k c_k |psi_k|^2.  Deterministic
+ * two-stage fp64 reduction.  cost_kind FQ_COST_F64 (costs = double*) or FQ_COST_U16
+ * (costs = uint16_t*, c = scale*v + offset). */
+int fq_expectation(const void *psi, const void *costs, int cost_kind, double scale,
+                   double offset, int64_t size, double *out_dev, double *scratch, void *stream);
+
+/* min / max of the decoded cost vector: out_dev[0] = min, out_dev[1] = max. */
+int fq_cost_minmax(const void *costs, int cost_kind, double scale, double offset, int64_t size,
+                   double *out_dev, double *scratch, void *stream);
+
+/* overlap numerator (statevec.py:100-111): *out_dev = sum_{c_k <= cutoff} |psi_k|^2
+ * (cutoff = min + tol, computed by the caller — globally for sharded runs). */
+int fq_masked_probability(const void *psi, const void *costs, int cost_kind, double scale,
+                          double offset, int64_t size, double cutoff, double *out_dev,
+                          double *scratch, void *stream);
+
+/* Lossless uint16 packing of a float64 diagonal (terms.py:155-175):
+ * out[k] = rint((c_k - offset)/scale); *bad_dev set nonzero if any level > 65535 or
+ * scale*v + offset != c_k bit-for-bit. */
+int fq_compact_u16(uint16_t *out, const double *costs, int64_t size, double scale, double offset,
+                   int *bad_dev, void *stream);
+
+/* ------------------------------------------------------------------ *
+ * Fused evolution (the B200 hot path)                                 *
+ * ------------------------------------------------------------------ */
+
+/* One layer of a fused program.  Layer l applies, in order,
+ * exp(-i gamma costs) (if apply_phase && gamma != 0) and then the mixer with
+ * angle beta restricted to qubit positions [q_lo, q_hi) (X / custom kinds).
+ * XY kinds always act on the full gate list of the local register. */
+typedef struct fq_layer {
+    double gamma;
+    double beta;
+    int apply_phase;
+    int q_lo, q_hi;
+} fq_layer;
+
+typedef struct fq_evolve_desc {
+    void *psi;            /* complex128[2^n] device, in/out                          */
+    int n;                /* local qubit count (log2 of the buffer length)           */
+    int cost_kind;        /* FQ_COST_F64 / FQ_COST_U16                               */
+    const void *costs;    /* device, same slicing as psi                             */
+    double cost_scale;    /* U16 decode: c = scale*v + offset                        */
+    double cost_offset;
+    int mixer;            /* FQ_MIXER_*                                              */
+    int n_layers;
+    const fq_layer *layers;   /* host array [n_layers]                               */
+    const double *su2;    /* host, FQ_MIXER_CUSTOM only: [n_layers][n][4] = a_re,a_im,b_re,b_im */
+    int init;             /* 0: psi holds the initial state; 1: start from |+>^n     */
+    double init_amp;      /* amplitude used when init == 1 (reference: 1/sqrt(2^n_global)) */
+    double *expectation_dev;  /* if non-NULL: sum_k c_k |psi_k|^2 of the final state  */
+    double *scratch;      /* device, >= FQ_SCRATCH_DOUBLES doubles                   */
+} fq_evolve_desc;
+
+/* Runs the whole p-layer program: phase fused into the first mixer pass of
+ * each layer, X/custom mixers applied 12 qubits per HBM pass in registers +
+ * shared memory, consecutive layers' passes fused across the layer boundary,
+ * expectation fused into the last pass.  States of n <= 12 qubits run the
+ * whole program inside one CTA. */
+int fq_qaoa_evolve(const fq_evolve_desc *desc, void *stream);
+
+/* Batched small-n evolution: `batch` independent parameter sets (gammas/betas
+ * host arrays [batch][p]) for the same cost vector, each evolved from |+>^n
+ * (or from psi_init if non-NULL, complex128[2^n] device) entirely on chip;
+ * writes expectations to out_dev[batch] and, if psi_out is non-NULL, final
+ * states to psi_out[batch][2^n].  n <= 12, X or custom-free kinds. */
+int fq_qaoa_evolve_batched(int n, int mixer, const void *costs, int cost_kind, double scale,
+                           double offset, int p, int batch, const double *gammas,
+                           const double *betas, const void *psi_init, void *psi_out,
+                           double *out_dev, void *stream);
+
+/* Number of HBM passes fq_qaoa_evolve will run for an X-mixer program (for the
+ * byte model in bench.py / DESIGN.md). */
+int fq_plan_x_passes(int n, int n_layers, const fq_layer *layers);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FQAOA_H */

@@ -1,0 +1,126 @@
+"""ctypes binding of libfqaoa.so (the C ABI declared in include/fqaoa.h).
+
+The product path has exactly one implementation: the sm_100a kernels in
+this library.  There is no CPU fallback — if the library or a CUDA device is
+missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfqaoa.so")
+
+FQ_OK, FQ_ERR_ARG, FQ_ERR_CUDA, FQ_ERR_UNSUPPORTED = 0, 1, 2, 3
+FQ_SCRATCH_DOUBLES = 4096
+MIXER_CODES = {"x": 0, "xy-ring": 1, "xy-complete": 2, "custom": 3}
+COST_F64, COST_U16 = 0, 1
+
+P, I64, D, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+
+
+class FqLayer(ctypes.Structure):
+    _fields_ = [("gamma", D), ("beta", D), ("apply_phase", I), ("q_lo", I), ("q_hi", I)]
+
+
+class FqEvolveDesc(ctypes.Structure):
+    _fields_ = [
+        ("psi", P), ("n", I), ("cost_kind", I), ("costs", P), ("cost_scale", D), ("cost_offset", D),
+        ("mixer", I), ("n_layers", I), ("layers", ctypes.POINTER(FqLayer)), ("su2", ctypes.POINTER(D)),
+        ("init", I), ("init_amp", D), ("expectation_dev", P), ("scratch", P),
+    ]
+
+
+_SIGS = {
+    "fq_version": ([], I),
+    "fq_last_error": ([], ctypes.c_char_p),
+    "fq_sm_count": ([], I),
+    "fq_su2_on_pairs": ([P, I64, D, D, D, D, I, P], I),
+    "fq_xy_on_pairs": ([P, I64, D, D, I, I, P], I),
+    "fq_swap_bits": ([P, I64, I, I, P], I),
+    "fq_phase_multiply": ([P, P, I64, D, P], I),
+    "fq_accumulate_terms": ([P, I64, P, P, I64, I64, P], I),
+    "fq_accumulate_terms_dyadic": ([P, I64, P, P, I64, I, I, I64, P], I),
+    "fq_precompute_levels_u16": ([P, I64, P, P, I64, I, I64, I64, I, P, P], I),
+    "fq_abs2_inplace": ([P, I64, P], I),
+    "fq_init_state": ([P, I64, I, D, I64, P], I),
+    "fq_expectation": ([P, P, I, D, D, I64, P, P, P], I),
+    "fq_cost_minmax": ([P, I, D, D, I64, P, P, P], I),
+    "fq_masked_probability": ([P, P, I, D, D, I64, D, P, P, P], I),
+    "fq_compact_u16": ([P, P, I64, D, D, P, P], I),
+    "fq_qaoa_evolve": ([ctypes.POINTER(FqEvolveDesc), P], I),
+    "fq_qaoa_evolve_batched": ([I, I, P, I, D, D, I, I, P, P, P, P, P, P], I),
+    "fq_plan_x_passes": ([I, I, ctypes.POINTER(FqLayer)], I),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str = LIB_PATH):
+    """Load libfqaoa.so (no CUDA device needed to load)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise ImportError(
+                    f"libfqaoa.so not found at {path}: build it with "
+                    "`python -m paper_2309_04841_b200._build` (there is no CPU fallback)"
+                )
+            lib = ctypes.CDLL(path)
+            for name, (args, res) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = res
+            _lib = lib
+    return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status == FQ_OK:
+        return
+    msg = (load().fq_last_error() or b"").decode(errors="replace")
+    if status == FQ_ERR_ARG:
+        raise ValueError(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: libfqaoa error {status}: {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def device() -> torch.device:
+    """The CUDA device the simulator runs on; raises if none (no CPU fallback)."""
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_2309_04841_b200 needs a CUDA device (B200, sm_100a); "
+            "there is no CPU fallback"
+        )
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+_scratch: dict[int, torch.Tensor] = {}
+
+
+def scratch() -> torch.Tensor:
+    dev = device()
+    buf = _scratch.get(dev.index)
+    if buf is None:
+        buf = torch.zeros(FQ_SCRATCH_DOUBLES, dtype=torch.float64, device=dev)
+        _scratch[dev.index] = buf
+    return buf
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()

@@ -1,0 +1,66 @@
+// Shared helpers for the libfqaoa kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fqaoa.h"
+
+namespace fq {
+
+// thread-local error text for fq_last_error()
+void set_error(const char *fmt, ...);
+
+#define FQ_CHECK_ARG(cond, ...)          \
+    do {                                 \
+        if (!(cond)) {                   \
+            ::fq::set_error(__VA_ARGS__); \
+            return FQ_ERR_ARG;           \
+        }                                \
+    } while (0)
+
+int cuda_status(cudaError_t e, const char *what);
+#define FQ_CUDA(call) \
+    do { int _s = ::fq::cuda_status((call), #call); if (_s) return _s; } while (0)
+#define FQ_LAUNCHED(what) \
+    do { int _s = ::fq::cuda_status(cudaGetLastError(), what); if (_s) return _s; } while (0)
+
+int sm_count();
+// grid size for a grid-stride kernel over `work` items of `per_block` each
+int grid_for(int64_t work, int per_block, int blocks_per_sm);
+
+inline bool is_pow2(int64_t x) { return x >= 2 && (x & (x - 1)) == 0; }
+inline int log2i(int64_t x) { int r = 0; while ((int64_t(1) << r) < x) ++r; return r; }
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// Decode of a uint16 level exactly as the reference's CompactCostVector.decode
+// (terms.py:133-135: scale * v + offset, two roundings, never contracted to FMA).
+__device__ __forceinline__ double decode_u16(uint16_t v, double scale, double offset) {
+    return __dadd_rn(__dmul_rn(scale, (double)v), offset);
+}
+
+// streaming (evict-first) 16-B global accesses: each amplitude is touched once per pass
+__device__ __forceinline__ double2 ld_stream(const double2 *p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stcs(p, v); }
+
+// Deterministic block reduction (fixed shuffle tree + fixed smem order).
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NT / 32; ++i) t += red[i];
+    }
+    return t;  // valid in thread 0
+}
+
+// Sums `count` partials in index order (one thread; count <= FQ_SCRATCH_DOUBLES).
+__global__ void k_sum_partials(const double *partials, int count, double *out);
+
+}  // namespace fq

@@ -1,0 +1,466 @@
+"""State sharding by global qubits (mirror of reference fastqaoa/distributed.py).
+
+Worker r owns global indices [r 2^(n-k), (r+1) 2^(n-k)) — the top k index
+bits are the "global" qubits (reference distributed.py:1-23, 51-54).  The
+only collective is the subchunk all-to-all V[a,b,c] -> V[b,a,c]
+(distributed.py:103-122): after it the former global qubits sit at local
+positions n-2k .. n-k-1, so an X-mixer layer is: local passes, exchange,
+one pass over k positions, exchange (Alg. 4).
+
+Two deployments of the same orchestration:
+
+* ``simulate_qaoa_distributed`` / ``ShardedState`` — K logical workers
+  inside one process on one GPU (the reference's own model, same API and
+  exchange counters); the exchange is a device transpose.
+* ``ShardedQaoaSimulator`` — one process per GPU (torchrun), shard-local
+  precompute by index offset (no n<=30 cap), exchange = NCCL all-to-all over
+  NVLink (``torch.distributed.all_to_all_single``, ncclAlltoAll), scalar
+  reductions = ``all_reduce``.  Local work is always libfqaoa.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from math import comb, sqrt
+from typing import Sequence
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib, instrumentation
+from .costs import DeviceCosts
+from .mixers import SU2, Mixer, complete_edges, ring_edges, run_program, su2_table
+from .qaoa import QaoaParams, QaoaResult, _initial_state, resolve_costs
+from .statevec import expectation_device, overlap_device
+from .terms import TermPolynomial
+
+
+def _validate_split(n: int, K: int) -> int:
+    """K = 2^k with 2k <= n (reference distributed.py:39-48; messages are test-matched)."""
+    k = K.bit_length() - 1
+    if K < 1 or (1 << k) != K:
+        raise ValueError(f"worker count {K} is not a power of two")
+    if 2 * k > n:
+        raise ValueError(
+            f"{K} workers split {n} qubits into subchunks smaller than one "
+            f"amplitude (need 2*log2(K) <= n)"
+        )
+    return k
+
+
+# ====================================================================== in-process
+@dataclass
+class ShardedState:
+    """K = 2^k shards of one state (reference distributed.py:51-62).  On the
+    device all shards are views of one [K, 2^(n-k)] buffer."""
+
+    n: int
+    k: int
+    shards: list
+    exchange_count: int = 0
+
+    @property
+    def K(self) -> int:
+        return 1 << self.k
+
+
+@dataclass
+class ShardedCosts:
+    """Cost diagonal sliced like the state (reference distributed.py:65-72)."""
+
+    n: int
+    k: int
+    shards: list
+
+
+def _as_device_vector(x) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(device=_lib.device()).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x)).to(_lib.device())
+
+
+def scatter(state, K: int) -> ShardedState:
+    """Split into K private shards (reference distributed.py:75-85)."""
+    size = state.numel() if isinstance(state, torch.Tensor) else np.asarray(state).size
+    n = (size - 1).bit_length()
+    if size != 1 << n:
+        raise ValueError(f"state length {size} is not a power of two")
+    k = _validate_split(n, K)
+    buf = _as_device_vector(np.asarray(state, dtype=np.complex128) if not isinstance(state, torch.Tensor) else state)
+    buf = buf.to(torch.complex128).clone().view(K, 1 << (n - k))
+    return ShardedState(n, k, list(buf.unbind(0)))
+
+
+def gather(sharded: ShardedState) -> np.ndarray:
+    """Concatenated host state (reference distributed.py:88-89)."""
+    return torch.cat([s.reshape(-1) for s in sharded.shards]).cpu().numpy()
+
+
+def shard_costs(costs, K: int) -> ShardedCosts:
+    """Slice a cost vector like the state (reference distributed.py:92-100)."""
+    if isinstance(costs, DeviceCosts):
+        n = costs.n
+        k = _validate_split(n, K)
+        return ShardedCosts(n, k, _slice_device_costs(costs, K))
+    arr = np.asarray(costs, dtype=np.float64)
+    n = (arr.size - 1).bit_length()
+    if arr.size != 1 << n:
+        raise ValueError(f"cost length {arr.size} is not a power of two")
+    k = _validate_split(n, K)
+    return ShardedCosts(n, k, _slice_device_costs(DeviceCosts.from_array(arr), K))
+
+
+def _slice_device_costs(dc: DeviceCosts, K: int) -> list[DeviceCosts]:
+    n_local = dc.n - (K.bit_length() - 1)
+    size = 1 << n_local
+    out = []
+    for r in range(K):
+        f = dc.f64[r * size:(r + 1) * size] if dc.f64 is not None else None
+        u = dc.u16[r * size:(r + 1) * size] if dc.u16 is not None else None
+        out.append(DeviceCosts(n_local, f64=f, u16=u, scale=dc.scale, offset=dc.offset))
+    return out
+
+
+def all_to_all_exchange(sharded: ShardedState) -> None:
+    """Subchunk j of worker i <-> subchunk i of worker j, in place; self-inverse
+    (reference distributed.py:103-122).  One device transpose of V[K,K,sub]."""
+    K = sharded.K
+    sub = 1 << (sharded.n - 2 * sharded.k)
+    V = torch.stack([s.reshape(K, sub) for s in sharded.shards])  # [a, b, c]
+    T = V.transpose(0, 1).contiguous()                             # [b, a, c]
+    for a in range(K):
+        sharded.shards[a].copy_(T[a].reshape(-1))
+    sharded.exchange_count += 1
+    instrumentation.bump("exchange")
+
+
+def _check_slicing(sharded: ShardedState, costs: ShardedCosts) -> None:
+    if (costs.n, costs.k) != (sharded.n, sharded.k):
+        raise ValueError("cost slicing does not match the state slicing")
+
+
+def apply_phase_distributed(sharded: ShardedState, costs: ShardedCosts, gamma: float) -> None:
+    """Per-shard phase, no communication (reference distributed.py:125-134)."""
+    _check_slicing(sharded, costs)
+    if gamma == 0.0:
+        return
+    n_local = sharded.n - sharded.k
+    for shard, dc in zip(sharded.shards, costs.shards):
+        run_program(shard, n_local, "x", [(gamma, 0.0, 1, 0, 0)], dc=dc)
+
+
+def _local_su2(sharded: ShardedState, us: Sequence[SU2], positions: range, offset: int) -> None:
+    """Apply us[pos + offset] at local positions ``positions`` on every shard."""
+    n_local = sharded.n - sharded.k
+    table = [SU2.identity()] * n_local
+    for pos in positions:
+        table[pos] = us[pos + offset]
+    t = su2_table([table])
+    for shard in sharded.shards:
+        run_program(shard, n_local, "custom", [(0.0, 0.0, 0, positions.start, positions.stop)], su2=t)
+
+
+def apply_uniform_su2_distributed(sharded: ShardedState, us: Sequence[SU2]) -> None:
+    """Local qubits, exchange, former global qubits at q-k, exchange — exactly
+    two exchanges (reference distributed.py:137-153)."""
+    n, k = sharded.n, sharded.k
+    if len(us) != n:
+        raise ValueError(f"expected {n} matrices, got {len(us)}")
+    _local_su2(sharded, us, range(0, n - k), 0)
+    all_to_all_exchange(sharded)
+    _local_su2(sharded, us, range(n - 2 * k, n - k), k)
+    all_to_all_exchange(sharded)
+
+
+def rx_layer_distributed(sharded: ShardedState, beta: float) -> None:
+    apply_uniform_su2_distributed(sharded, [SU2.rx(beta)] * sharded.n)
+
+
+def _xy_local(sharded: ShardedState, beta: float, lo: int, hi: int) -> None:
+    c, s = float(np.cos(beta)), float(np.sin(beta))
+    for shard in sharded.shards:
+        _lib.call("fq_xy_on_pairs", shard.data_ptr(), shard.numel(), c, s, lo, hi, _lib.stream())
+
+
+def _swap_local(sharded: ShardedState, lo: int, hi: int) -> None:
+    for shard in sharded.shards:
+        _lib.call("fq_swap_bits", shard.data_ptr(), shard.numel(), lo, hi, _lib.stream())
+
+
+def apply_xy_distributed(sharded: ShardedState, beta: float, i: int, j: int) -> None:
+    """XY gate on a sharded state (reference distributed.py:160-207): local
+    pairs directly; pairs touching a global qubit inside an exchange pair,
+    parking a subchunk-id partner at position 0 with swap_bits."""
+    n, k = sharded.n, sharded.k
+    if i == j:
+        raise ValueError(f"XY coupling needs two distinct qubits, got ({i}, {j})")
+    if not (0 <= i < n and 0 <= j < n):
+        raise ValueError(f"pair ({i}, {j}) out of range for {n} qubits")
+    lo, hi = min(i, j), max(i, j)
+    n_local = n - k
+    if hi < n_local:
+        _xy_local(sharded, beta, lo, hi)
+        return
+    b_start = n - 2 * k
+    parked = False
+    if b_start <= lo < n_local:
+        if b_start == 0:
+            raise ValueError(
+                f"pair ({i}, {j}) spans the subchunk-id and worker-id qubits; "
+                f"with 2*log2(K) == n there is no local position to stage it "
+                f"(use fewer workers)"
+            )
+        _swap_local(sharded, 0, lo)
+        lo, parked = 0, True
+    pos_lo = lo - k if lo >= n_local else lo
+    pos_hi = hi - k
+    all_to_all_exchange(sharded)
+    _xy_local(sharded, beta, min(pos_lo, pos_hi), max(pos_lo, pos_hi))
+    all_to_all_exchange(sharded)
+    if parked:
+        _swap_local(sharded, 0, min(i, j))
+
+
+def _mixer_layer_distributed(sharded: ShardedState, mixer: Mixer, beta: float) -> None:
+    if mixer.kind == "x":
+        rx_layer_distributed(sharded, beta)
+    elif mixer.kind in ("xy-ring", "xy-complete"):
+        edges = ring_edges(sharded.n) if mixer.kind == "xy-ring" else complete_edges(sharded.n)
+        for i, j in edges:
+            apply_xy_distributed(sharded, beta, i, j)
+    else:
+        apply_uniform_su2_distributed(sharded, mixer.su2_factory(beta))
+
+
+def expectation_distributed(sharded: ShardedState, costs: ShardedCosts) -> float:
+    """Sum of per-shard partials (reference distributed.py:228-237)."""
+    _check_slicing(sharded, costs)
+    parts = [expectation_device(s, c) for s, c in zip(sharded.shards, costs.shards)]
+    return float(torch.cat(parts).cpu().numpy().sum())
+
+
+def overlap_distributed(sharded: ShardedState, costs: ShardedCosts, tol: float = 0.0) -> float:
+    """Global min, masked sum, clamp (reference distributed.py:240-252)."""
+    _check_slicing(sharded, costs)
+    cutoff = min(c.minmax()[0] for c in costs.shards) + tol
+    parts = [overlap_device(s, c, cutoff) for s, c in zip(sharded.shards, costs.shards)]
+    return min(max(float(torch.cat(parts).cpu().numpy().sum()), 0.0), 1.0)
+
+
+@dataclass
+class DistributedResult:
+    """Evolved sharded state + sliced diagonal (reference distributed.py:255-277)."""
+
+    sharded: ShardedState
+    sharded_costs: ShardedCosts
+    costs_device: DeviceCosts = field(repr=False)
+
+    @property
+    def exchange_count(self) -> int:
+        return self.sharded.exchange_count
+
+    @property
+    def costs(self) -> np.ndarray:
+        return self.costs_device.host()
+
+    def statevector(self) -> np.ndarray:
+        return gather(self.sharded)
+
+    def expectation(self) -> float:
+        return expectation_distributed(self.sharded, self.sharded_costs)
+
+    def overlap(self, tol: float = 0.0) -> float:
+        return overlap_distributed(self.sharded, self.sharded_costs, tol=tol)
+
+    def to_result(self) -> QaoaResult:
+        state = torch.cat([s.reshape(-1) for s in self.sharded.shards]).clone()
+        return QaoaResult(state, self.costs_device)
+
+
+def simulate_qaoa_distributed(problem, params: QaoaParams, K: int, mixer: "str | Mixer" = "x",
+                              initial=None) -> DistributedResult:
+    """K logical workers on the current GPU (reference distributed.py:280-296).
+    For the X mixer, phase + local qubits run as one fused program per shard."""
+    dc, n = resolve_costs(problem)
+    mixer = Mixer.parse(mixer)
+    k = _validate_split(n, K)
+    state, init = _initial_state(n, mixer, initial)
+    if init:
+        _lib.call("fq_init_state", state.data_ptr(), state.numel(), -1, 1.0 / sqrt(float(1 << n)), 0, _lib.stream())
+    sharded = ShardedState(n, k, list(state.view(K, -1).unbind(0)))
+    sc = ShardedCosts(n, k, _slice_device_costs(dc, K))
+    n_local = n - k
+    for gamma, beta in zip(params.gammas, params.betas):
+        if mixer.kind == "x" and k > 0:
+            for shard, c in zip(sharded.shards, sc.shards):
+                run_program(shard, n_local, "x", [(gamma, beta, 1, 0, n_local)], dc=c)
+            all_to_all_exchange(sharded)
+            for shard in sharded.shards:
+                run_program(shard, n_local, "x", [(0.0, beta, 0, n_local - k, n_local)])
+            all_to_all_exchange(sharded)
+        else:
+            apply_phase_distributed(sharded, sc, gamma)
+            _mixer_layer_distributed(sharded, mixer, beta)
+    return DistributedResult(sharded, sc, dc)
+
+
+# ====================================================================== one process per GPU
+class ShardedQaoaSimulator:
+    """One rank per GPU; this rank holds global indices
+    [rank 2^(n-k), (rank+1) 2^(n-k)).  Launch with torchrun; the process
+    group must be NCCL for CUDA shards.
+
+    Per X layer (Alg. 4): [phase + local qubits] fused passes, NCCL all-to-all,
+    one pass over the k former-global positions, NCCL all-to-all.  The
+    exchange double-buffers (receive into a second shard buffer, then swap
+    pointers) when memory allows, else runs in bounded chunks."""
+
+    def __init__(self, poly: TermPolynomial, group=None, mixer: "str | Mixer" = "x",
+                 compact: bool = True, keep_f64: bool | None = None, chunk_bytes: int | None = None,
+                 local_ops=None):
+        self.group = group
+        self.K = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.n = poly.n
+        self.k = _validate_split(self.n, self.K)
+        self.n_local = self.n - self.k
+        self.mixer = Mixer.parse(mixer)
+        self.ops = local_ops if local_ops is not None else CudaLocalOps()
+        base = self.rank << self.n_local
+        if keep_f64 is None:
+            keep_f64 = self.ops.fits(self.n_local, 8 + 16 * 2 + 2)
+        self.costs = self.ops.precompute(poly, base, self.n_local, compact, keep_f64)
+        instrumentation.bump("precompute")
+        self.exchange_count = 0
+        self.chunk_bytes = chunk_bytes
+        self._state = None
+        self._spare = None
+
+    # ------------------------------------------------------------------ exchange
+    def exchange(self, shard: torch.Tensor) -> torch.Tensor:
+        """V[a,b,c] -> V[b,a,c] across ranks; returns the tensor now holding the shard."""
+        K = self.K
+        if K == 1:
+            return shard
+        full_ok = self.chunk_bytes is None and (self._spare is not None or self.ops.fits_bytes(shard.numel() * 16))
+        if full_ok:
+            if self._spare is None or self._spare.numel() != shard.numel():
+                self._spare = torch.empty_like(shard)
+            dist.all_to_all_single(self._spare, shard, group=self.group)
+            out, self._spare = self._spare, shard
+        else:
+            # bounded staging: column block [c0, c1) of every subchunk per round;
+            # row j of the send block goes to rank j, row a of the receive
+            # block came from rank a, i.e. V_me[a, c] = V_a[me, c].
+            sub = shard.numel() // K
+            V = shard.view(K, sub)
+            piece = max(1, min(sub, (self.chunk_bytes or (256 << 20)) // (16 * K)))
+            for c0 in range(0, sub, piece):
+                c1 = min(sub, c0 + piece)
+                send = V[:, c0:c1].contiguous()
+                recv = torch.empty_like(send)
+                dist.all_to_all_single(recv, send, group=self.group)
+                V[:, c0:c1].copy_(recv)
+            out = shard
+        self.exchange_count += 1
+        instrumentation.bump("exchange")
+        return out
+
+    # ------------------------------------------------------------------ evolution
+    def initial_state(self, initial_weight: int | None = None) -> torch.Tensor:
+        if initial_weight is None:
+            return self.ops.uniform(self.n, self.n_local)
+        return self.ops.hamming(self.n, initial_weight, self.rank << self.n_local, self.n_local)
+
+    def simulate_qaoa(self, gammas: Sequence[float], betas: Sequence[float], initial_weight: int | None = None,
+                      expectation: bool = True) -> float | None:
+        """Evolve; returns the global expectation (all-reduced) if requested."""
+        params = QaoaParams(tuple(gammas), tuple(betas))
+        if self.mixer.preserves_hamming_weight and initial_weight is None:
+            raise ValueError("XY mixers need initial_weight (Hamming-weight sector)")
+        if self.mixer.kind != "x":
+            raise NotImplementedError("multi-process sharding supports the X mixer (XY: simulate_qaoa_distributed)")
+        nl, k = self.n_local, self.k
+        psi = self.ops.empty(nl) if initial_weight is None else self.initial_state(initial_weight)
+        init = initial_weight is None
+        amp = 1.0 / sqrt(float(2 ** self.n)) if init else 0.0
+        for li, (g, b) in enumerate(zip(params.gammas, params.betas)):
+            self.ops.program(psi, nl, "x", [(g, b, 1, 0, nl)], self.costs, init=init and li == 0, init_amp=amp)
+            if k > 0:
+                psi = self.exchange(psi)
+                self.ops.program(psi, nl, "x", [(0.0, b, 0, nl - k, nl)], None)
+                psi = self.exchange(psi)
+        if params.p == 0 and init:
+            psi = self.ops.uniform(self.n, nl)
+        self._state = psi
+        if not expectation:
+            return None
+        return self.expectation()
+
+    def expectation(self) -> float:
+        local = self.ops.expectation(self._state, self.costs)
+        dist.all_reduce(local, op=dist.ReduceOp.SUM, group=self.group)
+        return float(local.item())
+
+    def overlap(self, tol: float = 0.0) -> float:
+        lo = self.ops.min_cost(self.costs)
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=self.group)
+        part = self.ops.masked_probability(self._state, self.costs, float(lo.item()) + tol)
+        dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.group)
+        return min(max(float(part.item()), 0.0), 1.0)
+
+    @property
+    def shard(self) -> torch.Tensor:
+        return self._state
+
+
+class CudaLocalOps:
+    """Shard-local work for ShardedQaoaSimulator: always libfqaoa on the
+    rank's CUDA device (no fallback)."""
+
+    def fits(self, n_local: int, bytes_per_amp: int) -> bool:
+        free, _ = torch.cuda.mem_get_info(_lib.device())
+        return (1 << n_local) * bytes_per_amp < 0.9 * free
+
+    def fits_bytes(self, nbytes: int) -> bool:
+        free, _ = torch.cuda.mem_get_info(_lib.device())
+        return nbytes < 0.9 * free
+
+    def precompute(self, poly, base: int, n_local: int, compact: bool, keep_f64: bool) -> DeviceCosts:
+        return DeviceCosts.from_polynomial(poly, compact=compact, keep_f64=keep_f64, index_base=base,
+                                           n_local=n_local)
+
+    def empty(self, n_local: int) -> torch.Tensor:
+        return torch.empty(1 << n_local, dtype=torch.complex128, device=_lib.device())
+
+    def uniform(self, n: int, n_local: int) -> torch.Tensor:
+        psi = self.empty(n_local)
+        _lib.call("fq_init_state", psi.data_ptr(), psi.numel(), -1, 1.0 / sqrt(float(2 ** n)), 0, _lib.stream())
+        return psi
+
+    def hamming(self, n: int, weight: int, base: int, n_local: int) -> torch.Tensor:
+        psi = self.empty(n_local)
+        _lib.call("fq_init_state", psi.data_ptr(), psi.numel(), weight, 1.0 / sqrt(comb(n, weight)), base,
+                  _lib.stream())
+        return psi
+
+    def program(self, psi, n_local, kind, layers, costs, init=False, init_amp=0.0):
+        run_program(psi, n_local, kind, layers, dc=costs, init=init, init_amp=init_amp)
+
+    def expectation(self, psi, costs) -> torch.Tensor:
+        return expectation_device(psi, costs)
+
+    def min_cost(self, costs) -> torch.Tensor:
+        return torch.tensor([costs.minmax()[0]], dtype=torch.float64, device=_lib.device())
+
+    def masked_probability(self, psi, costs, cutoff) -> torch.Tensor:
+        return overlap_device(psi, costs, cutoff)
+
+
+__all__ = [
+    "ShardedState", "ShardedCosts", "scatter", "gather", "shard_costs", "all_to_all_exchange",
+    "apply_phase_distributed", "apply_uniform_su2_distributed", "rx_layer_distributed", "apply_xy_distributed",
+    "expectation_distributed", "overlap_distributed", "DistributedResult", "simulate_qaoa_distributed",
+    "ShardedQaoaSimulator", "CudaLocalOps",
+]

@@ -1,0 +1,268 @@
+"""Layered QAOA evolution on a B200 (mirror of reference fastqaoa/qaoa.py).
+
+The cost diagonal is evaluated once per problem on the GPU and stays
+resident; ``simulate_qaoa`` enqueues one fused program (libfqaoa
+``fq_qaoa_evolve``): phase and mixer layers batched 12 qubits per HBM pass,
+with the objective sum c|psi|^2 folded into the last pass.  ``get_*``
+accessors return host (CPU) values, as in the paper's API.
+"""
+
+from __future__ import annotations
+
+from collections import OrderedDict
+from dataclasses import dataclass
+from math import sqrt
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib, instrumentation
+from .costs import DeviceCosts
+from .mixers import Mixer, run_program
+from .statevec import expectation_device, num_qubits, overlap_device
+from .terms import TermPolynomial, _check_fits
+
+
+@dataclass(frozen=True)
+class QaoaParams:
+    """Per-layer angle pairs (reference qaoa.py:31-60)."""
+
+    gammas: tuple[float, ...]
+    betas: tuple[float, ...]
+
+    def __post_init__(self) -> None:
+        object.__setattr__(self, "gammas", tuple(float(g) for g in self.gammas))
+        object.__setattr__(self, "betas", tuple(float(b) for b in self.betas))
+        if len(self.gammas) != len(self.betas):
+            raise ValueError(f"{len(self.gammas)} gammas but {len(self.betas)} betas")
+
+    @property
+    def p(self) -> int:
+        return len(self.gammas)
+
+    @classmethod
+    def from_flat(cls, x: Sequence[float]) -> QaoaParams:
+        x = np.asarray(x, dtype=np.float64)
+        if x.size % 2:
+            raise ValueError(f"flat parameter vector has odd length {x.size}")
+        p = x.size // 2
+        return cls(tuple(x[:p]), tuple(x[p:]))
+
+    def to_flat(self) -> np.ndarray:
+        return np.array(self.gammas + self.betas, dtype=np.float64)
+
+
+class QaoaResult:
+    """Final state (device) plus the cost diagonal it was evolved under
+    (reference qaoa.py:63-68).  ``state`` / ``costs`` are host numpy views
+    copied on first access; ``state_device`` / ``costs_device`` stay on the GPU."""
+
+    def __init__(self, state_device: torch.Tensor, costs_device: DeviceCosts,
+                 expectation_dev: torch.Tensor | None = None):
+        self.state_device = state_device
+        self.costs_device = costs_device
+        self._expectation_dev = expectation_dev
+        self._state_host: np.ndarray | None = None
+
+    @property
+    def state(self) -> np.ndarray:
+        if self._state_host is None:
+            self._state_host = self.state_device.cpu().numpy()
+        return self._state_host
+
+    @property
+    def costs(self) -> np.ndarray:
+        return self.costs_device.host()
+
+    @property
+    def n(self) -> int:
+        return self.costs_device.n
+
+    def _mutated(self) -> None:
+        self._expectation_dev = None
+        self._state_host = None
+
+
+_COST_MEMO: "OrderedDict[TermPolynomial, DeviceCosts]" = OrderedDict()
+_MEMO_SIZE = 32
+
+
+def _cached_device_costs(poly: TermPolynomial) -> DeviceCosts:
+    """Process-wide memo of device diagonals (reference qaoa.py:71-75, lru 32)."""
+    dc = _COST_MEMO.get(poly)
+    if dc is not None:
+        _COST_MEMO.move_to_end(poly)
+        return dc
+    _check_fits(poly.n, 8, "cost vector")
+    dc = DeviceCosts.from_polynomial(poly)
+    instrumentation.bump("precompute")
+    _COST_MEMO[poly] = dc
+    while len(_COST_MEMO) > _MEMO_SIZE:
+        _COST_MEMO.popitem(last=False)
+    return dc
+
+
+def resolve_costs(problem) -> tuple[DeviceCosts, int]:
+    """Device diagonal + qubit count for a polynomial (memoised) or a ready
+    2^n vector (reference qaoa.py:78-87)."""
+    if isinstance(problem, TermPolynomial):
+        return _cached_device_costs(problem), problem.n
+    if isinstance(problem, DeviceCosts):
+        return problem, problem.n
+    dc = DeviceCosts.from_array(problem)
+    return dc, dc.n
+
+
+def _initial_state(n: int, mixer: Mixer, initial) -> tuple[torch.Tensor, bool]:
+    """(device state, generate-|+>-in-kernel flag) — reference qaoa.py:90-103."""
+    dev = _lib.device()
+    if initial is not None:
+        if isinstance(initial, torch.Tensor):
+            if initial.numel() != 1 << n:
+                raise ValueError(f"initial state has {initial.numel()} amplitudes, expected {1 << n}")
+            return initial.to(device=dev, dtype=torch.complex128).clone().contiguous(), False
+        arr = np.array(initial, dtype=np.complex128)
+        if arr.size != 1 << n:
+            raise ValueError(f"initial state has {arr.size} amplitudes, expected {1 << n}")
+        return torch.from_numpy(arr.reshape(-1)).to(dev), False
+    if mixer.preserves_hamming_weight:
+        raise ValueError(
+            "XY mixers act within a fixed-popcount sector; pass an initial "
+            "state explicitly (see statevec.hamming_weight_state)"
+        )
+    _check_fits(n, 16, "state vector")
+    return torch.empty(1 << n, dtype=torch.complex128, device=dev), True
+
+
+def _evolve(dc: DeviceCosts, n: int, mixer: Mixer, params: QaoaParams, initial,
+            out: torch.Tensor | None = None) -> QaoaResult:
+    state, init = _initial_state(n, mixer, initial)
+    if out is not None and init:
+        state = out
+    layers = [(g, b, 1, 0, n) for g, b in zip(params.gammas, params.betas)]
+    exp_dev = torch.empty(1, dtype=torch.float64, device=state.device)
+    run_program(state, n, mixer.kind, layers, dc=dc, su2=mixer.su2_table(params.betas, n),
+                init=init, init_amp=1.0 / sqrt(float(1 << n)), expectation_out=exp_dev)
+    return QaoaResult(state, dc, exp_dev)
+
+
+class QaoaSimulator:
+    """Simulator bound to one problem; the cost diagonal is computed once, on
+    the GPU, at construction (reference qaoa.py:106-166)."""
+
+    def __init__(self, n: int | None = None, *, terms=None, costs=None, mixer: "str | Mixer" = "x") -> None:
+        if (terms is None) == (costs is None):
+            raise ValueError("pass exactly one of terms= or costs=")
+        if terms is not None:
+            if not isinstance(terms, TermPolynomial):
+                if n is None:
+                    raise ValueError("a plain term list needs n")
+                terms = TermPolynomial.from_pairs(n, terms)
+            _check_fits(terms.n, 8, "cost vector")
+            self._dc = DeviceCosts.from_polynomial(terms)
+            instrumentation.bump("precompute")
+            self.n = terms.n
+        else:
+            self._dc = costs if isinstance(costs, DeviceCosts) else DeviceCosts.from_array(costs)
+            self.n = self._dc.n
+        if n is not None and n != self.n:
+            raise ValueError(f"n={n} disagrees with problem size {self.n}")
+        self.mixer = Mixer.parse(mixer)
+        self._buffer: torch.Tensor | None = None
+
+    @property
+    def device_costs(self) -> DeviceCosts:
+        return self._dc
+
+    def get_cost_diagonal(self) -> np.ndarray:
+        return self._dc.host()
+
+    def simulate_qaoa(self, gammas: Sequence[float], betas: Sequence[float], initial=None,
+                      reuse_buffer: bool = False) -> QaoaResult:
+        """Run the layered evolution; the result's state lives on the GPU.
+
+        ``reuse_buffer=True`` evolves into one simulator-owned state buffer
+        (objective loops at large n: no per-call allocation; the previous
+        result's state is overwritten)."""
+        params = QaoaParams(tuple(gammas), tuple(betas))
+        out = None
+        if reuse_buffer:
+            if self._buffer is None:
+                self._buffer = torch.empty(1 << self.n, dtype=torch.complex128, device=_lib.device())
+            out = self._buffer
+        return _evolve(self._dc, self.n, self.mixer, params, initial, out=out)
+
+    def simulate_qaoa_batched(self, gammas, betas) -> np.ndarray:
+        """Expectations of many parameter sets at once (n <= 12: each set
+        runs in its own CTA, one launch).  gammas, betas: [batch, p]."""
+        g = np.ascontiguousarray(gammas, dtype=np.float64)
+        b = np.ascontiguousarray(betas, dtype=np.float64)
+        if g.ndim != 2 or g.shape != b.shape:
+            raise ValueError("gammas and betas must both be [batch, p]")
+        if self.n > 12 or self.mixer.kind == "custom":
+            return np.array([self.get_expectation(self.simulate_qaoa(gg, bb)) for gg, bb in zip(g, b)])
+        if self.mixer.preserves_hamming_weight:
+            raise ValueError("XY mixers need an explicit initial state; use simulate_qaoa")
+        batch, p = g.shape
+        out = torch.empty(batch, dtype=torch.float64, device=_lib.device())
+        kind, cp, scale, offset = self._dc.kernel_view()
+        chunk = max(1, 512 // max(p, 1))
+        for s in range(0, batch, chunk):
+            e = min(batch, s + chunk)
+            gs, bs = np.ascontiguousarray(g[s:e]), np.ascontiguousarray(b[s:e])
+            _lib.call("fq_qaoa_evolve_batched", self.n, _lib.MIXER_CODES[self.mixer.kind], cp, kind, scale, offset,
+                      p, e - s, gs.ctypes.data, bs.ctypes.data, None, None, out[s:].data_ptr(), _lib.stream())
+        return out.cpu().numpy()
+
+    def get_statevector(self, result: QaoaResult) -> np.ndarray:
+        return result.state
+
+    def get_probabilities(self, result: QaoaResult, preserve_state: bool = True) -> np.ndarray:
+        psi = result.state_device
+        work = psi.clone() if preserve_state else psi
+        _lib.call("fq_abs2_inplace", work.data_ptr(), work.numel(), _lib.stream())
+        if not preserve_state:
+            result._mutated()
+        return torch.view_as_real(work)[:, 0].cpu().numpy()
+
+    def get_expectation(self, result: QaoaResult, costs=None) -> float:
+        if costs is None:
+            if result._expectation_dev is not None:
+                return float(result._expectation_dev.item())
+            dc = result.costs_device
+        else:
+            dc = costs if isinstance(costs, DeviceCosts) else DeviceCosts.from_array(costs, compact=False)
+            if dc.size != result.state_device.numel():
+                raise ValueError(
+                    f"state has {result.state_device.numel()} amplitudes but cost vector has {dc.size} entries")
+        return float(expectation_device(result.state_device, dc).item())
+
+    def get_overlap(self, result: QaoaResult, costs=None, tol: float = 0.0) -> float:
+        if costs is None:
+            dc = result.costs_device
+        else:
+            dc = costs if isinstance(costs, DeviceCosts) else DeviceCosts.from_array(costs, compact=False)
+            if dc.size != result.state_device.numel():
+                raise ValueError(
+                    f"state has {result.state_device.numel()} amplitudes but cost vector has {dc.size} entries")
+        lo, _ = dc.minmax()
+        total = float(overlap_device(result.state_device, dc, lo + tol).item())
+        return min(max(total, 0.0), 1.0)
+
+
+def simulate_qaoa(problem, params: QaoaParams, mixer: "str | Mixer" = "x", initial=None) -> QaoaResult:
+    """One-shot evolution; the device diagonal is memoised per polynomial
+    (reference qaoa.py:169-182)."""
+    dc, n = resolve_costs(problem)
+    return _evolve(dc, n, Mixer.parse(mixer), params, initial)
+
+
+def qaoa_objective(problem, params: QaoaParams, mixer: "str | Mixer" = "x", initial=None) -> float:
+    """Expected cost of the evolved state (reference qaoa.py:185-194)."""
+    result = simulate_qaoa(problem, params, mixer=mixer, initial=initial)
+    return float(result._expectation_dev.item())
+
+
+__all__ = ["QaoaParams", "QaoaResult", "QaoaSimulator", "simulate_qaoa", "qaoa_objective", "resolve_costs",
+           "num_qubits"]

@@ -1,0 +1,162 @@
+"""CPU-only checks: the C-ABI library loads and exports everything
+include/fqaoa.h declares, the host-side planner, and the host mirror of the
+reference API (validation, encodings, error contract).  No kernel launches."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2309_04841_b200 import _lib
+from paper_2309_04841_b200.mixers import SU2, Mixer, complete_edges, ring_edges
+from paper_2309_04841_b200.problems import Graph, labs_terms, maxcut_terms, portfolio_terms, triangle_graph
+from paper_2309_04841_b200.qaoa import QaoaParams
+from paper_2309_04841_b200.terms import (CompactRangeError, Term, TermPolynomial, _dyadic, compact_costs,
+                                         load_terms, save_terms, term_arrays)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "fqaoa.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fq_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 19
+    for s in syms:
+        assert hasattr(lib, s), f"libfqaoa.so does not export {s}"
+    assert set(syms) == set(_lib.EXPORTED), "ctypes signature table out of sync with fqaoa.h"
+
+
+def test_library_is_sm100a():
+    path = _lib.LIB_PATH
+    data = open(path, "rb").read()
+    assert b"sm_100a" in data or b"sm_100" in data
+
+
+def test_version_and_error_plumbing_without_gpu():
+    lib = _lib.load()
+    assert lib.fq_version() == 1
+    # argument validation happens before any CUDA call
+    st = lib.fq_su2_on_pairs(None, 3, 1.0, 0.0, 0.0, 0.0, 0, None)
+    assert st == _lib.FQ_ERR_ARG
+    assert b"bad buffer" in lib.fq_last_error()
+    with pytest.raises(ValueError, match="p_lo < p_hi"):
+        _lib.check(lib.fq_xy_on_pairs(ctypes.c_void_p(16), 16, 1.0, 0.0, 2, 1, None), "xy")
+
+
+def test_no_cpu_fallback():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _lib.device()
+    from paper_2309_04841_b200 import QaoaSimulator
+
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        QaoaSimulator(terms=labs_terms(4))
+
+
+def _plan(n, p):
+    layers = (_lib.FqLayer * p)(*[_lib.FqLayer(0.1, 0.2, 1, 0, n) for _ in range(p)])
+    return _lib.load().fq_plan_x_passes(n, p, layers)
+
+
+def test_pass_planner_counts():
+    # 3 qubit groups at n = 26 (12 + 7 + 7) -> 1 + 2p fused passes
+    assert _plan(26, 10) == 21
+    assert _plan(26, 1) == 3
+    # n = 13..22: two groups -> p + 1 passes
+    assert _plan(16, 4) == 5
+    assert _plan(22, 10) == 11
+    # n = 34 local 31: 12 + 10 + 9 -> 3 groups
+    assert _plan(31, 10) == 21
+    assert _plan(12, 4) == 1  # resident
+
+
+# ------------------------------------------------------------------ host mirror of the reference
+def test_term_validation():
+    assert Term(1.0, (3, 1)).support == (1, 3)
+    with pytest.raises(ValueError, match="duplicate"):
+        Term(1.0, (1, 1))
+    with pytest.raises(ValueError, match="negative"):
+        Term(1.0, (-1,))
+    with pytest.raises(ValueError, match="does not fit"):
+        TermPolynomial(2, (Term(1.0, (2,)),))
+    assert Term(1.0, (0, 3)).mask == 9
+
+
+def test_labs_and_maxcut_match_oracle_generators():
+    for n in (2, 3, 7, 12, 26):
+        ours = [(t.weight, t.support) for t in labs_terms(n).terms]
+        assert ours == O.labs_terms(n)
+    assert len(labs_terms(26).terms) == 1378
+    assert len(labs_terms(34).terms) == 3128
+    tri = maxcut_terms(triangle_graph())
+    assert [(t.weight, t.support) for t in tri.terms] == [(0.5, (0, 1)), (0.5, (0, 2)), (0.5, (1, 2)), (-1.5, ())]
+
+
+def test_dyadic_detection():
+    iw, s, tot = _dyadic(np.array([2.0, 1.0, -3.0]))
+    assert s == 0 and list(iw) == [2, 1, -3] and tot == 6
+    iw, s, tot = _dyadic(np.array([0.5, 0.5, -1.5]))
+    assert s == 1 and list(iw) == [1, 1, -3]
+    iw, s, tot = _dyadic(np.array([0.1]))
+    assert iw is None
+    ta = term_arrays(portfolio_terms(8))
+    assert ta.iweights is None  # float weights -> sequential f64 kernel
+
+
+def test_compact_costs_host_format(golden):
+    for name in ("labs12", "labs14", "cubic12"):
+        cc = compact_costs(golden[f"diag/{name}"])
+        np.testing.assert_array_equal(cc.values, golden[f"compact/{name}/values"])
+        assert (cc.scale, cc.offset) == tuple(golden[f"compact/{name}/scale_offset"])
+        np.testing.assert_array_equal(cc.decode(), golden[f"diag/{name}"])
+    with pytest.raises(CompactRangeError):
+        compact_costs(np.array([0.0, 1.0, np.pi, 70000.0]))
+
+
+def test_terms_json_round_trip(tmp_path):
+    poly = labs_terms(6)
+    p = tmp_path / "t.json"
+    save_terms(poly, str(p))
+    assert load_terms(str(p)) == poly
+
+
+def test_params_and_mixers():
+    with pytest.raises(ValueError, match="gammas"):
+        QaoaParams((0.1,), (0.1, 0.2))
+    assert QaoaParams.from_flat(QaoaParams((0.1, 0.2), (0.3, 0.4)).to_flat()) == QaoaParams((0.1, 0.2), (0.3, 0.4))
+    with pytest.raises(ValueError, match="odd"):
+        QaoaParams.from_flat([1.0, 2.0, 3.0])
+    assert ring_edges(5) == [(0, 1), (2, 3), (1, 2), (3, 4), (4, 0)]
+    assert complete_edges(3) == [(0, 1), (0, 2), (1, 2)]
+    with pytest.raises(ValueError, match="unknown"):
+        Mixer("zz")
+    with pytest.raises(ValueError, match="factory"):
+        Mixer("custom")
+    assert Mixer.parse("xy-ring").preserves_hamming_weight
+    with pytest.raises(ValueError, match="special unitary"):
+        SU2(1.0, 1.0)
+    np.testing.assert_allclose(SU2.rx(0.3).matrix(), [[np.cos(0.3), -1j * np.sin(0.3)],
+                                                      [-1j * np.sin(0.3), np.cos(0.3)]])
+
+
+def test_graph_validation():
+    with pytest.raises(ValueError, match="duplicate"):
+        Graph.from_edges(3, [(0, 1), (1, 0)])
+    with pytest.raises(ValueError, match="self-loop"):
+        Graph.from_edges(3, [(1, 1)])
+    edges = [tuple(map(int, l.split())) for l in open(os.path.join(ROOT, "tests", "golden", "maxcut26.edges"))
+             if not l.startswith("#")]
+    g = Graph.from_edges(26, edges)
+    assert len(g.edges) == 39 and len(maxcut_terms(g).terms) == 40
