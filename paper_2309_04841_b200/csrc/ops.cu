@@ -116,7 +116,8 @@ __global__ void k_abs2(double2 *__restrict__ psi, int64_t size) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < size;
          k += (int64_t)gridDim.x * blockDim.x) {
         const double2 x = psi[k];
-        psi[k] = make_double2(x.x * x.x + x.y * x.y, 0.0);
+        // re*re + im*im with the reference's two roundings (no FMA contraction)
+        psi[k] = make_double2(__dadd_rn(__dmul_rn(x.x, x.x), __dmul_rn(x.y, x.y)), 0.0);
     }
 }
 

@@ -131,8 +131,11 @@ def _initial_state(n: int, mixer: Mixer, initial) -> tuple[torch.Tensor, bool]:
             "XY mixers act within a fixed-popcount sector; pass an initial "
             "state explicitly (see statevec.hamming_weight_state)"
         )
-    _check_fits(n, 16, "state vector")
-    return torch.empty(1 << n, dtype=torch.complex128, device=dev), True
+    try:
+        return torch.empty(1 << n, dtype=torch.complex128, device=dev), True
+    except torch.OutOfMemoryError as exc:
+        raise MemoryError(f"state vector for n={n} does not fit in device memory "
+                          f"(shard it: simulate_qaoa_distributed / ShardedQaoaSimulator)") from exc
 
 
 def _evolve(dc: DeviceCosts, n: int, mixer: Mixer, params: QaoaParams, initial,
