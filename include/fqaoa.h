@@ -153,6 +153,8 @@ typedef struct fq_evolve_desc {
     const void *costs;    /* device, same slicing as psi                             */
     double cost_scale;    /* U16 decode: c = scale*v + offset                        */
     double cost_offset;
+    int cost_levels;      /* U16: 1 + largest level present (0 = unknown); sizes the
+                             phase tables (< 16384 -> table lookups, else sincos)    */
     int mixer;            /* FQ_MIXER_*                                              */
     int n_layers;
     const fq_layer *layers;   /* host array [n_layers]                               */
@@ -183,6 +185,10 @@ int fq_qaoa_evolve_batched(int n, int mixer, const void *costs, int cost_kind, d
 /* Number of HBM passes fq_qaoa_evolve will run for an X-mixer program (for the
  * byte model in bench.py / DESIGN.md). */
 int fq_plan_x_passes(int n, int n_layers, const fq_layer *layers);
+
+/* Runtime switches (testing / A-B measurement): "tma" = 1 (default) stages
+ * tiles with cp.async.bulk.tensor, 0 forces the register-load pass kernel. */
+int fq_set_option(const char *name, int value);
 
 #ifdef __cplusplus
 }

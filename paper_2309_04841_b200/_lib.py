@@ -31,7 +31,7 @@ class FqLayer(ctypes.Structure):
 class FqEvolveDesc(ctypes.Structure):
     _fields_ = [
         ("psi", P), ("n", I), ("cost_kind", I), ("costs", P), ("cost_scale", D), ("cost_offset", D),
-        ("mixer", I), ("n_layers", I), ("layers", ctypes.POINTER(FqLayer)), ("su2", ctypes.POINTER(D)),
+        ("cost_levels", I), ("mixer", I), ("n_layers", I), ("layers", ctypes.POINTER(FqLayer)), ("su2", ctypes.POINTER(D)),
         ("init", I), ("init_amp", D), ("expectation_dev", P), ("scratch", P),
     ]
 
@@ -56,6 +56,7 @@ _SIGS = {
     "fq_qaoa_evolve": ([ctypes.POINTER(FqEvolveDesc), P], I),
     "fq_qaoa_evolve_batched": ([I, I, P, I, D, D, I, I, P, P, P, P, P, P], I),
     "fq_plan_x_passes": ([I, I, ctypes.POINTER(FqLayer)], I),
+    "fq_set_option": ([ctypes.c_char_p, I], I),
 }
 
 EXPORTED = tuple(_SIGS)

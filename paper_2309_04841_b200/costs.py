@@ -21,8 +21,9 @@ class DeviceCosts:
     """Cost diagonal of one (shard of a) problem on the current CUDA device."""
 
     def __init__(self, n: int, f64: torch.Tensor | None = None, u16: torch.Tensor | None = None,
-                 scale: float = 1.0, offset: float = 0.0):
+                 scale: float = 1.0, offset: float = 0.0, levels: int = 0):
         self.n = n
+        self.levels = int(levels)  # uint16: 1 + largest level (sizes the phase tables); 0 = unknown
         self.f64 = f64
         self.u16 = u16
         self.scale = float(scale)
@@ -77,6 +78,7 @@ class DeviceCosts:
                       bad.data_ptr(), _lib.stream())
             if int(bad.item()) == 0:
                 self.u16, self.scale, self.offset = u16, scale, lo
+                self.levels = int(round((hi - lo) / scale)) + 1
                 return True
         return False
 
@@ -106,6 +108,7 @@ class DeviceCosts:
         if int(bad.item()) != 0:
             return False
         self.u16 = out
+        self.levels = 2 * ta.abs_sum + 1
         self.scale = 2.0 ** -ta.shift
         self.offset = float(lo) * self.scale
         return True

@@ -34,6 +34,11 @@
 #include <cstring>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace fq {
@@ -67,9 +72,23 @@ struct PassParams {
     int phase_at;             // 1: before set A, 2: between A and B
     int init;                 // generate |+> instead of loading
     int expect;               // accumulate sum c|x|^2 in the last round
-    unsigned char maskA[5], maskB[5];
+    int table_hi;             // U16 phase: rows of the high table (0 -> sincos of the decoded cost)
+    unsigned char maskA[8], maskB[8];  // per round: register bits getting set A / set B butterflies
     CoefSet A, B;
+    // TMA staging (k_pass_tma): tensor-map dims in ascending physical order
+    int tma_rank;             // state map rank (dim 0 = doubles)
+    int tma_outer_shift[5];   // outer dims: coordinate = (tile >> shift) & ((1 << bits) - 1)
+    int tma_outer_bits[5];    // 0 for tile dims (coordinate 0)
+    int cost_tma;             // costs staged by TMA (same dims) instead of LDG
+    int cost_rank;
+    int cost_outer_shift[5];
+    int cost_outer_bits[5];
+    int probe_l2;             // development probe: tiles alias a 64 MiB L2-resident set (compute-bound timing)
 };
+
+constexpr int kTableLo = 64;     // low-table rows (6 level bits)
+constexpr int kMaxTableHi = 256; // high-table rows -> levels < 16384 use tables
+constexpr int kCopies = 8;       // one copy per 16-B bank group: conflict-free random lookups
 
 template <int PAT>
 __device__ __forceinline__ int tile_bit_of_reg(int j) {
@@ -83,7 +102,34 @@ __device__ __forceinline__ int tidx(int tid, int i) {
     return (tid & 15) | (i << 4) | ((tid >> 4) << 8);
 }
 
-__device__ __forceinline__ int swz(int e) { return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7); }
+// Transpose scratch layout: tile index e lives at slot e + (e >> 4) (one pad
+// entry per 16).  For all three register patterns the thread part and the
+// register part of the slot are additive (slot = pat_base(tid) + pat_step(i)),
+// so every access is [base register + immediate], and a quarter-warp's eight
+// 16-B accesses always fall in eight distinct bank groups.
+constexpr int kTilePadded = kTile + kTile / 16;
+
+template <int PAT>
+__device__ __forceinline__ int pat_base(int tid) {
+    if (PAT == PAT8) return tid + (tid >> 4);
+    if (PAT == PAT0) return 17 * tid;
+    return (tid & 15) + 272 * (tid >> 4);
+}
+template <int PAT>
+__host__ __device__ constexpr int pat_step(int i) {
+    return PAT == PAT8 ? 272 * i : (PAT == PAT0 ? i : 17 * i);
+}
+// raw (unpadded, TMA box order) index: thread part + register part, additive
+template <int PAT>
+__device__ __forceinline__ int raw_base(int tid) {
+    if (PAT == PAT8) return tid;
+    if (PAT == PAT0) return tid << 4;
+    return (tid & 15) + ((tid >> 4) << 8);
+}
+template <int PAT>
+__host__ __device__ constexpr int raw_step(int i) {
+    return PAT == PAT8 ? (i << 8) : (PAT == PAT0 ? i : (i << 4));
+}
 
 // physical offset of this thread's element 0 for pattern PAT
 template <int PAT>
@@ -112,13 +158,15 @@ __device__ __forceinline__ void reg_offsets(const PassParams &P, long long (&o)[
 
 template <int PAT>
 __device__ __forceinline__ void transpose_out(double2 *sm, const double2 (&v)[kRegs], int tid) {
+    double2 *p = sm + pat_base<PAT>(tid);
 #pragma unroll
-    for (int i = 0; i < kRegs; ++i) sm[swz(tidx<PAT>(tid, i))] = v[i];
+    for (int i = 0; i < kRegs; ++i) p[pat_step<PAT>(i)] = v[i];
 }
 template <int PAT>
 __device__ __forceinline__ void transpose_in(const double2 *sm, double2 (&v)[kRegs], int tid) {
+    const double2 *p = sm + pat_base<PAT>(tid);
 #pragma unroll
-    for (int i = 0; i < kRegs; ++i) v[i] = sm[swz(tidx<PAT>(tid, i))];
+    for (int i = 0; i < kRegs; ++i) v[i] = p[pat_step<PAT>(i)];
 }
 
 template <int FROM, int TO>
@@ -178,17 +226,27 @@ __device__ __forceinline__ void butterflies(double2 (&v)[kRegs], const CoefSet &
 }
 
 // ---- phase
+// exp(-i gamma c) for a float64 cost: the reference's angle = gamma * c, then sincos.
+__device__ __forceinline__ double2 phase_f64(double c, double gamma) {
+    double s, co;
+    sincos(gamma * c, &s, &co);
+    return make_double2(co, -s);
+}
+
+// exp(-i gamma c) for a uint16 level v, c = scale*v + offset:
+// T_hi[v >> 6] * T_lo[v & 63], each table replicated once per 16-B bank group
+// (copy = lane & 7) so a quarter-warp's random lookups never conflict.
+__device__ __forceinline__ double2 phase_u16(unsigned v, const PassParams &P, const double2 *tlo, const double2 *thi) {
+    if (P.table_hi == 0) return phase_f64(decode_u16((uint16_t)v, P.cost_scale, P.cost_offset), P.gamma);
+    const int cp = threadIdx.x & (kCopies - 1);
+    return cmul(thi[(v >> 6) * kCopies + cp], tlo[(v & 63) * kCopies + cp]);
+}
+
 template <int COST>
-__device__ __forceinline__ double2 phase_factor(const void *costs, long long k, double gamma, const double2 *tlo,
+__device__ __forceinline__ double2 phase_factor(const PassParams &P, long long k, const double2 *tlo,
                                                 const double2 *thi) {
-    if (COST == FQ_COST_F64) {
-        double s, c;
-        sincos(gamma * static_cast<const double *>(costs)[k], &s, &c);
-        return make_double2(c, -s);
-    } else {
-        const unsigned v = static_cast<const uint16_t *>(costs)[k];
-        return cmul(thi[v >> 8], tlo[v & 255]);
-    }
+    if (COST == FQ_COST_F64) return phase_f64(static_cast<const double *>(P.costs)[k], P.gamma);
+    return phase_u16(static_cast<const uint16_t *>(P.costs)[k], P, tlo, thi);
 }
 
 template <int COST>
@@ -197,103 +255,810 @@ __device__ __forceinline__ double cost_value(const void *costs, long long k, dou
     return decode_u16(static_cast<const uint16_t *>(costs)[k], scale, offset);
 }
 
-// e^{-i gamma c} tables for uint16 levels: c = scale*(256 h + l) + offset
-__device__ __forceinline__ void build_phase_tables(double2 *tlo, double2 *thi, double gamma, double scale,
+// e^{-i gamma c} tables for uint16 levels: c = scale*(64 h + l) + offset
+__device__ __forceinline__ void build_phase_tables(double2 *tlo, double2 *thi, int n_hi, double gamma, double scale,
                                                    double offset) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    for (int i = threadIdx.x; i < kTableLo + n_hi; i += blockDim.x) {
         double s, c;
-        sincos(gamma * (scale * (double)i), &s, &c);
-        tlo[i] = make_double2(c, -s);
-        sincos(gamma * (scale * (double)(256 * i) + offset), &s, &c);
-        thi[i] = make_double2(c, -s);
+        if (i < kTableLo) sincos(gamma * (scale * (double)i), &s, &c);
+        else sincos(gamma * (scale * (double)(64 * (i - kTableLo)) + offset), &s, &c);
+        double2 *row = (i < kTableLo) ? tlo + i * kCopies : thi + (i - kTableLo) * kCopies;
+#pragma unroll
+        for (int k = 0; k < kCopies; ++k) row[k] = make_double2(c, -s);
     }
 }
 
-template <int MIX, int COST, int PAT>
-__device__ __forceinline__ void run_round(const PassParams &P, int r, double2 (&v)[kRegs], long long base,
-                                          long long thr, const double2 *tlo, const double2 *thi) {
+// One register round: [phase] butterflies(A) [phase] butterflies(B).
+// `cost(i)` yields the raw cost entry (double, or uint16 level) of element i.
+template <int MIX, int COST, int PAT, typename CostFn>
+__device__ __forceinline__ void run_round(const PassParams &P, int r, double2 (&v)[kRegs], CostFn cost,
+                                          const double2 *tlo, const double2 *thi) {
     const bool ph = (P.phase_round == r);
     if (ph && P.phase_at == 1) {
-        long long o[kRegs];
-        reg_offsets<PAT>(P, o);
 #pragma unroll
-        for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase_factor<COST>(P.costs, base + thr + o[i], P.gamma, tlo, thi));
+        for (int i = 0; i < kRegs; ++i)
+            v[i] = cmul(v[i], COST == FQ_COST_F64 ? phase_f64(cost(i), P.gamma) : phase_u16((unsigned)cost(i), P, tlo, thi));
     }
     if (P.maskA[r]) butterflies<MIX, PAT>(v, P.A, P.maskA[r]);
     if (ph && P.phase_at == 2) {
-        long long o[kRegs];
-        reg_offsets<PAT>(P, o);
 #pragma unroll
-        for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase_factor<COST>(P.costs, base + thr + o[i], P.gamma, tlo, thi));
+        for (int i = 0; i < kRegs; ++i)
+            v[i] = cmul(v[i], COST == FQ_COST_F64 ? phase_f64(cost(i), P.gamma) : phase_u16((unsigned)cost(i), P, tlo, thi));
     }
     if (P.maskB[r]) butterflies<MIX, PAT>(v, P.B, P.maskB[r]);
 }
 
-template <int MIX, int COST, int NR>
-__global__ void __launch_bounds__(kThreads, 2) k_tile_pass(const __grid_constant__ PassParams P) {
+template <int COST>
+__device__ __forceinline__ double global_cost(const PassParams &P, long long k) {
+    if (COST == FQ_COST_F64) return static_cast<const double *>(P.costs)[k];
+    return (double)static_cast<const uint16_t *>(P.costs)[k];
+}
+
+template <int COST>
+__device__ __forceinline__ double decode_cost(const PassParams &P, double raw) {
+    if (COST == FQ_COST_F64) return raw;
+    return decode_u16((uint16_t)raw, P.cost_scale, P.cost_offset);
+}
+
+// tile number -> base address: insert a zero at every tile bit position
+__device__ __forceinline__ long long tile_base(const PassParams &P, long long t) {
+    long long base = P.probe_l2 ? (t & 1023) : t;
+#pragma unroll
+    for (int j = 0; j < kTileBits; ++j) {
+        const int p = P.tile_pos[j];
+        base = ((base >> p) << (p + 1)) | (base & ((1LL << p) - 1));
+    }
+    return base;
+}
+
+__device__ __forceinline__ size_t table_doubles2(int n_hi) { return (size_t)(kTableLo + n_hi) * kCopies; }
+
+// ---------------------------------------------------------------- 16-amplitude pass (default)
+// Register-load pass, 256 threads x 16 amplitudes per 2^12 tile, 2 CTAs/SM.
+// Everything that varies between passes of one program is a template
+// parameter, so the tile loop contains no runtime branches on it and the
+// kernel body stays I-cache resident:
+//   PH: 0 no phase, 1 phase before set A (round 0), 2 phase between set A and
+//       set B (round 2, then rounds 3-4 finish set B: a fused layer boundary);
+//   MA, MB: RX form of sets A/B (0: (1, tan b), 1: (cot b, 1)); MB = 2: no set
+//       B; MB = 3: set B present, form chosen at run time (rare: gamma = 0).
+//   PROBE: development memory-pattern probe (load + store only).
+template <int MIX, int M, int PAT>
+__device__ __forceinline__ void bfly16(double2 (&v)[kRegs], const CoefSet &C, int mask) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (!((mask >> j) & 1)) continue;
+        if (MIX == MIX_RX) {
+            const double r = C.r;
+            if (M == 0) {
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i)
+                    if (!(i & (1 << j))) bfly_rx0(v[i], v[i | (1 << j)], r);
+            } else {
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i)
+                    if (!(i & (1 << j))) bfly_rx1(v[i], v[i | (1 << j)], r);
+            }
+        } else {
+            const int tb = tile_bit_of_reg<PAT>(j);
+            const double2 a = C.a[tb], b = C.b[tb];
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i)
+                if (!(i & (1 << j))) bfly_su2(v[i], v[i | (1 << j)], a, b);
+        }
+    }
+}
+
+template <int MIX, int M, int PAT>
+__device__ __forceinline__ void bfly16_set(double2 (&v)[kRegs], const CoefSet &C, int mask) {
+    if (M == 3) {  // run-time form (set B without a separating phase)
+        if (C.mode == 0) bfly16<MIX, 0, PAT>(v, C, mask);
+        else bfly16<MIX, 1, PAT>(v, C, mask);
+    } else {
+        bfly16<MIX, M, PAT>(v, C, mask);
+    }
+}
+
+__device__ __noinline__ double2 phase_sincos_u16(unsigned v, double scale, double offset, double gamma) {
+    return phase_f64(decode_u16((uint16_t)v, scale, offset), gamma);
+}
+
+template <int COST>
+__device__ __forceinline__ double2 phase16(const PassParams &P, double raw, const double2 *tlo, const double2 *thi) {
+    if (COST == FQ_COST_F64) return phase_f64(raw, P.gamma);
+    const unsigned v = (unsigned)raw;
+    if (P.table_hi == 0) return phase_sincos_u16(v, P.cost_scale, P.cost_offset, P.gamma);
+    const int cp = threadIdx.x & (kCopies - 1);
+    return cmul(thi[(v >> 6) * kCopies + cp], tlo[(v & 63) * kCopies + cp]);
+}
+
+template <int MIX, int COST, int PH, int MA, int MB, int PROBE>
+__global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ PassParams P) {
     extern __shared__ double2 smem[];
     double2 *tile = smem;
-    double2 *tlo = smem + kTile;
-    double2 *thi = tlo + 256;
+    double2 *tlo = smem + kTilePadded;
+    double2 *thi = tlo + kTableLo * kCopies;
     __shared__ double red[kThreads / 32];
     const int tid = threadIdx.x;
+    constexpr bool HAS_B = MB != 2;
 
-    if (COST == FQ_COST_U16 && P.phase_round >= 0) {
-        build_phase_tables(tlo, thi, P.gamma, P.cost_scale, P.cost_offset);
+    if (COST == FQ_COST_U16 && PH != 0 && !PROBE) {
+        if (P.table_hi > 0) build_phase_tables(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
         __syncthreads();
     }
     const long long thr8 = thread_offset<PAT8>(P, tid);
-    const long long thr0 = thread_offset<PAT0>(P, tid);
     const long long thr4 = thread_offset<PAT4>(P, tid);
     double eacc = 0.0;
 
     for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
-        // tile number -> base address: insert a zero at every tile bit position
-        long long base = t;
-#pragma unroll
-        for (int j = 0; j < kTileBits; ++j) {
-            const int p = P.tile_pos[j];
-            base = ((base >> p) << (p + 1)) | (base & ((1LL << p) - 1));
-        }
+        const long long base = tile_base(P, t);
         double2 v[kRegs];
+        double raw[kRegs];  // cost entries of the phase round (loaded with the state)
         {
             long long o[kRegs];
             reg_offsets<PAT8>(P, o);
-            if (P.init) {
+            if (P.init || PROBE == 2) {
 #pragma unroll
-                for (int i = 0; i < kRegs; ++i) v[i] = make_double2(P.init_amp, 0.0);
+                for (int i = 0; i < kRegs; ++i) v[i] = make_double2(P.init_amp + i, (double)t);
             } else {
 #pragma unroll
                 for (int i = 0; i < kRegs; ++i) v[i] = ld_stream(P.psi + base + thr8 + o[i]);
             }
+            if (PH == 1) {
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) raw[i] = global_cost<COST>(P, base + thr8 + o[i]);
+            }
         }
-        run_round<MIX, COST, PAT8>(P, 0, v, base, thr8, tlo, thi);
-        transpose<PAT8, PAT0>(tile, v, tid);
-        run_round<MIX, COST, PAT0>(P, 1, v, base, thr0, tlo, thi);
-        transpose<PAT0, PAT4>(tile, v, tid);
-        run_round<MIX, COST, PAT4>(P, 2, v, base, thr4, tlo, thi);
-        if (NR == 5) {
-            transpose<PAT4, PAT0>(tile, v, tid);
-            run_round<MIX, COST, PAT0>(P, 3, v, base, thr0, tlo, thi);
-            transpose<PAT0, PAT8>(tile, v, tid);
-            run_round<MIX, COST, PAT8>(P, 4, v, base, thr8, tlo, thi);
+        if (PH == 2) {
+            long long o[kRegs];
+            reg_offsets<PAT4>(P, o);
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i) raw[i] = global_cost<COST>(P, base + thr4 + o[i]);
         }
-        constexpr int LAST = (NR == 5) ? PAT8 : PAT4;
-        const long long thrL = (NR == 5) ? thr8 : thr4;
+        if (PROBE != 1) {
+            // round 0: tile bits 8-11
+            if (PH == 1) {
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase16<COST>(P, raw[i], tlo, thi));
+            }
+            bfly16_set<MIX, MA, PAT8>(v, P.A, P.maskA[0]);
+            if (HAS_B && PH != 2) bfly16_set<MIX, MB, PAT8>(v, P.B, P.maskB[0]);
+            transpose<PAT8, PAT0>(tile, v, tid);
+            // round 1: tile bits 0-3
+            bfly16_set<MIX, MA, PAT0>(v, P.A, P.maskA[1]);
+            if (HAS_B && PH != 2) bfly16_set<MIX, MB, PAT0>(v, P.B, P.maskB[1]);
+            transpose<PAT0, PAT4>(tile, v, tid);
+            // round 2: tile bits 4-7
+            bfly16_set<MIX, MA, PAT4>(v, P.A, P.maskA[2]);
+            if (PH == 2) {
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase16<COST>(P, raw[i], tlo, thi));
+            }
+            if (HAS_B) bfly16_set<MIX, MB, PAT4>(v, P.B, P.maskB[2]);
+            if (PH == 2) {
+                transpose<PAT4, PAT0>(tile, v, tid);
+                bfly16_set<MIX, MB, PAT0>(v, P.B, P.maskB[3]);
+                transpose<PAT0, PAT8>(tile, v, tid);
+                bfly16_set<MIX, MB, PAT8>(v, P.B, P.maskB[4]);
+            }
+        }
+        constexpr int LAST = (PH == 2 || PROBE == 1) ? PAT8 : PAT4;
+        const long long thrL = (PH == 2 || PROBE == 1) ? thr8 : thr4;
         long long o[kRegs];
         reg_offsets<LAST>(P, o);
         const double fs = P.final_scale;
+        if (PROBE == 2) {  // on-chip work only: keep the result live, store (almost) nothing
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i) acc += v[i].x * fs + v[i].y;
+            if (acc == 1.2345e300) st_stream(P.psi + base + thrL, make_double2(acc, 0.0));
+            continue;
+        }
 #pragma unroll
         for (int i = 0; i < kRegs; ++i) {
             double2 x = v[i];
-            if (MIX == MIX_RX) x = make_double2(x.x * fs, x.y * fs);
-            if (P.expect) eacc += cost_value<COST>(P.costs, base + thrL + o[i], P.cost_scale, P.cost_offset) *
-                                  (x.x * x.x + x.y * x.y);
+            if (MIX == MIX_RX && PROBE != 1) x = make_double2(x.x * fs, x.y * fs);
+            if (P.expect) eacc += decode_cost<COST>(P, global_cost<COST>(P, base + thrL + o[i])) * (x.x * x.x + x.y * x.y);
             st_stream(P.psi + base + thrL + o[i], x);
         }
     }
     if (P.expect) {
         const double s = block_sum<kThreads>(eacc, red);
+        if (tid == 0) P.partials[blockIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------- TMA-staged pass
+// One persistent CTA per SM.  Tiles (and their cost slices) stream into two
+// shared-memory stages with cp.async.bulk.tensor; tile i+1 is in flight while
+// tile i is transformed in registers (its stage buffer doubling as the
+// transpose scratch).  Results go back with streaming 16-B stores.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load(void *dst, const CUtensorMap *map, int rank, const int *c, uint64_t *bar) {
+    const uint32_t d = smem_u32(dst), b = smem_u32(bar);
+    const uint64_t m = reinterpret_cast<uint64_t>(map);
+    switch (rank) {
+        case 1:
+            asm volatile("cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];"
+                         ::"r"(d), "l"(m), "r"(c[0]), "r"(b) : "memory");
+            break;
+        case 2:
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                         ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(b) : "memory");
+            break;
+        case 3:
+            asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                         ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(b) : "memory");
+            break;
+        case 4:
+            asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                         ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(b) : "memory");
+            break;
+        default:
+            asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                         ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(b) : "memory");
+            break;
+    }
+}
+
+__device__ __forceinline__ void tile_coords(long long t, int rank, const int *shift, const int *bits, int *c) {
+#pragma unroll
+    for (int d = 0; d < 5; ++d)
+        c[d] = (d < rank && bits[d] > 0) ? (int)((t >> shift[d]) & ((1LL << bits[d]) - 1)) : 0;
+}
+
+__device__ __forceinline__ void tma_store(const CUtensorMap *map, int rank, const int *c, const void *src) {
+    const uint32_t sa = smem_u32(src);
+    const uint64_t m = reinterpret_cast<uint64_t>(map);
+    switch (rank) {
+        case 1:
+            asm volatile("cp.async.bulk.tensor.1d.global.shared::cta.bulk_group [%0, {%1}], [%2];"
+                         ::"l"(m), "r"(c[0]), "r"(sa) : "memory");
+            break;
+        case 2:
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                         ::"l"(m), "r"(c[0]), "r"(c[1]), "r"(sa) : "memory");
+            break;
+        case 3:
+            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                         ::"l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(sa) : "memory");
+            break;
+        case 4:
+            asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
+                         ::"l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(sa) : "memory");
+            break;
+        default:
+            asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];"
+                         ::"l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(sa) : "memory");
+            break;
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+constexpr int kStageEntries = kTilePadded;              // double2 per state stage (padded transpose layout)
+constexpr int kStateStageBytes = kTilePadded * 16;
+constexpr uint32_t kStateTxBytes = kTile * 16;
+
+template <int COST>
+__host__ __device__ constexpr int cost_stage_bytes() { return COST == FQ_COST_F64 ? kTile * 8 : kTile * 2; }
+
+template <int COST>
+__host__ __device__ constexpr size_t tma_smem_bytes(int n_hi) {
+    return 2 * (size_t)kStateStageBytes + 2 * (size_t)cost_stage_bytes<COST>() +
+           (COST == FQ_COST_U16 ? (size_t)(kTableLo + n_hi) * kCopies * 16 : 0) + 64;
+}
+
+// Persistent CTA per SM, two stages.  Stage b: TMA load (state + costs) ->
+// round 0 reads the raw box -> transposes in the padded layout -> last round
+// writes the raw box -> TMA store -> (store has read it) next TMA load.
+template <int MIX, int COST, int NR>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_pass_tma(const __grid_constant__ PassParams P, const __grid_constant__ CUtensorMap tm_state,
+               const __grid_constant__ CUtensorMap tm_cost) {
+    extern __shared__ __align__(128) double2 sm2[];
+    double2 *const tlo = sm2 + 2 * kStageEntries + (2 * cost_stage_bytes<COST>()) / 16;
+    double2 *const thi = tlo + kTableLo * kCopies;
+    uint64_t *const bar = reinterpret_cast<uint64_t *>(
+        sm2 + 2 * kStageEntries + (2 * cost_stage_bytes<COST>()) / 16 +
+        (COST == FQ_COST_U16 ? (kTableLo + P.table_hi) * kCopies : 0));
+    __shared__ double red[kThreads / 32];
+    const int tid = threadIdx.x;
+
+    const bool need_cost = (P.phase_round >= 0) || P.expect;
+    const bool stage_cost = need_cost && P.cost_tma;
+    const bool load_state = !P.init;
+    const uint32_t tx = (load_state ? kStateTxBytes : 0) + (stage_cost ? cost_stage_bytes<COST>() : 0);
+
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (COST == FQ_COST_U16 && P.phase_round >= 0 && P.table_hi > 0)
+        build_phase_tables(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
+    __syncthreads();
+
+    auto issue = [&](long long t, int b) {
+        if (tx == 0) return;
+        mbar_expect_tx(&bar[b], tx);
+        int c[5];
+        if (load_state) {
+            tile_coords(P.probe_l2 ? (t & 1023) : t, P.tma_rank, P.tma_outer_shift, P.tma_outer_bits, c);
+            tma_load(sm2 + b * kStageEntries, &tm_state, P.tma_rank, c, &bar[b]);
+        }
+        if (stage_cost) {
+            tile_coords(P.probe_l2 ? (t & 1023) : t, P.cost_rank, P.cost_outer_shift, P.cost_outer_bits, c);
+            tma_load(sm2 + 2 * kStageEntries + b * (cost_stage_bytes<COST>() / 16), &tm_cost, P.cost_rank, c, &bar[b]);
+        }
+    };
+    if (tid == 0) {
+        if (blockIdx.x < P.n_tiles) issue(blockIdx.x, 0);
+        if (blockIdx.x + gridDim.x < P.n_tiles) issue(blockIdx.x + gridDim.x, 1);
+    }
+
+    double eacc = 0.0;
+    int it = 0;
+    for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x, ++it) {
+        const int b = it & 1;
+        double2 *const buf = sm2 + b * kStageEntries;
+        const void *const cs = sm2 + 2 * kStageEntries + b * (cost_stage_bytes<COST>() / 16);
+        if (tx) mbar_wait(&bar[b], (it >> 1) & 1);
+        long long base = -1;  // global base, only for the LDG cost fallback
+        auto scost = [&](auto pat_tag) {
+            constexpr int PAT = decltype(pat_tag)::value;
+            return [&](int i) -> double {
+                if (P.cost_tma) {
+                    const int e = raw_base<PAT>(tid) + raw_step<PAT>(i);
+                    if (COST == FQ_COST_F64) return static_cast<const double *>(cs)[e];
+                    return (double)static_cast<const uint16_t *>(cs)[e];
+                }
+                if (base < 0) base = tile_base(P, t);
+                long long o[kRegs];
+                reg_offsets<PAT>(P, o);
+                return global_cost<COST>(P, base + thread_offset<PAT>(P, tid) + o[i]);
+            };
+        };
+        double2 v[kRegs];
+        if (P.init) {
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i) v[i] = make_double2(P.init_amp, 0.0);
+        } else {
+            const double2 *p = buf + raw_base<PAT8>(tid);
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i) v[i] = p[raw_step<PAT8>(i)];
+        }
+        run_round<MIX, COST, PAT8>(P, 0, v, scost(std::integral_constant<int, PAT8>{}), tlo, thi);
+        __syncthreads();  // every thread has consumed the raw stage layout
+        transpose<PAT8, PAT0>(buf, v, tid);
+        run_round<MIX, COST, PAT0>(P, 1, v, scost(std::integral_constant<int, PAT0>{}), tlo, thi);
+        transpose<PAT0, PAT4>(buf, v, tid);
+        run_round<MIX, COST, PAT4>(P, 2, v, scost(std::integral_constant<int, PAT4>{}), tlo, thi);
+        if (NR == 5) {
+            transpose<PAT4, PAT0>(buf, v, tid);
+            run_round<MIX, COST, PAT0>(P, 3, v, scost(std::integral_constant<int, PAT0>{}), tlo, thi);
+            transpose<PAT0, PAT8>(buf, v, tid);
+            run_round<MIX, COST, PAT8>(P, 4, v, scost(std::integral_constant<int, PAT8>{}), tlo, thi);
+        }
+        constexpr int LAST = (NR == 5) ? PAT8 : PAT4;
+        auto lastcost = scost(std::integral_constant<int, LAST>{});
+        const double fs = P.final_scale;
+        double2 *q = buf + raw_base<LAST>(tid);
+#pragma unroll
+        for (int i = 0; i < kRegs; ++i) {
+            double2 x = v[i];
+            if (MIX == MIX_RX) x = make_double2(x.x * fs, x.y * fs);
+            if (P.expect) eacc += decode_cost<COST>(P, lastcost(i)) * (x.x * x.x + x.y * x.y);
+            q[raw_step<LAST>(i)] = x;
+        }
+        fence_proxy_async();  // make this thread's raw-box writes visible to the TMA engine
+        __syncthreads();
+        if (tid == 0) {
+            int c[5];
+            tile_coords(P.probe_l2 ? (t & 1023) : t, P.tma_rank, P.tma_outer_shift, P.tma_outer_bits, c);
+            tma_store(&tm_state, P.tma_rank, c, buf);
+            if (t + 2 * (long long)gridDim.x < P.n_tiles) {
+                tma_store_wait_read();  // the store has read stage b: reload it
+                issue(t + 2 * (long long)gridDim.x, b);
+            }
+        }
+    }
+    if (tid == 0) tma_store_wait_all();
+    if (P.expect) {
+        const double s = block_sum<kThreads>(eacc, red);
+        if (tid == 0) P.partials[blockIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------- 8-amplitude pass (default)
+// 512 threads x 8 amplitudes per 2^12 tile, two CTAs per SM (32 warps): the
+// pass is latency-bound at 16-amplitude / 8-warp occupancy, so it trades one
+// more shared-memory transpose for 4x the resident warps.  Register round r
+// holds tile bits [f_r, f_r + 3) with f = 9, 0, 3, 6 (round 0 = global load
+// pattern: lanes on tile bits 0-4, coalesced; round 3 = store pattern, also
+// lanes on bits 0-4).  A fused two-layer pass with a phase between runs the
+// rounds 0 1 2 3 | 3 2 1 0.
+constexpr int k8Threads = 512;
+constexpr int k8Regs = 8;
+constexpr int k8Padded = kTile + kTile / 8;  // slot = e + (e >> 3)
+
+__host__ __device__ constexpr int f8(int r) { return r == 0 ? 9 : 3 * (r - 1); }
+
+template <int F>
+__device__ __forceinline__ int p8_base(int tid) {
+    const int low = tid & ((1 << F) - 1), high = tid >> F;
+    return low + (low >> 3) + 9 * (high << F);
+}
+template <int F>
+__host__ __device__ constexpr int p8_step(int i) { return (i << F) + ((i << F) >> 3); }
+template <int F>
+__device__ __forceinline__ int raw8_base(int tid) {
+    const int low = tid & ((1 << F) - 1), high = tid >> F;
+    return low | (high << (F + 3));
+}
+template <int F>
+__host__ __device__ constexpr int raw8_step(int i) { return i << F; }
+
+// physical offset of this thread's element 0 when tile bits [F, F+3) are in registers
+template <int F>
+__device__ __forceinline__ long long thr8_offset(const PassParams &P, int tid) {
+    long long off = 0;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        const int tb = j < F ? j : j + 3;
+        if ((tid >> j) & 1) off += 1LL << P.tile_pos[tb];
+    }
+    return off;
+}
+template <int F>
+__device__ __forceinline__ void reg8_offsets(const PassParams &P, long long (&o)[k8Regs]) {
+    const long long s0 = 1LL << P.tile_pos[F], s1 = 1LL << P.tile_pos[F + 1], s2 = 1LL << P.tile_pos[F + 2];
+    o[0] = 0; o[1] = s0; o[2] = s1; o[3] = s0 + s1;
+    o[4] = s2; o[5] = s2 + s0; o[6] = s2 + s1; o[7] = s2 + s1 + s0;
+}
+
+template <int F>
+__device__ __forceinline__ void t8_out(double2 *sm, const double2 (&v)[k8Regs], int tid) {
+    double2 *p = sm + p8_base<F>(tid);
+#pragma unroll
+    for (int i = 0; i < k8Regs; ++i) p[p8_step<F>(i)] = v[i];
+}
+template <int F>
+__device__ __forceinline__ void t8_in(const double2 *sm, double2 (&v)[k8Regs], int tid) {
+    const double2 *p = sm + p8_base<F>(tid);
+#pragma unroll
+    for (int i = 0; i < k8Regs; ++i) v[i] = p[p8_step<F>(i)];
+}
+template <int FROM, int TO>
+__device__ __forceinline__ void t8(double2 *sm, double2 (&v)[k8Regs], int tid) {
+    t8_out<FROM>(sm, v, tid);
+    __syncthreads();
+    t8_in<TO>(sm, v, tid);
+    __syncthreads();
+}
+
+template <int MIX, int F>
+__device__ __forceinline__ void bfly8(double2 (&v)[k8Regs], const CoefSet &C, int mask) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        if (!((mask >> j) & 1)) continue;
+        if (MIX == MIX_RX) {
+            const double r = C.r;
+            if (C.mode == 0) {
+#pragma unroll
+                for (int i = 0; i < k8Regs; ++i)
+                    if (!(i & (1 << j))) bfly_rx0(v[i], v[i | (1 << j)], r);
+            } else {
+#pragma unroll
+                for (int i = 0; i < k8Regs; ++i)
+                    if (!(i & (1 << j))) bfly_rx1(v[i], v[i | (1 << j)], r);
+            }
+        } else {
+            const double2 a = C.a[F + j], b = C.b[F + j];
+#pragma unroll
+            for (int i = 0; i < k8Regs; ++i)
+                if (!(i & (1 << j))) bfly_su2(v[i], v[i | (1 << j)], a, b);
+        }
+    }
+}
+
+// one round: [phase] A [phase] B ; costs read from global at this round's pattern
+template <int MIX, int COST, int F>
+__device__ __forceinline__ void round8(const PassParams &P, int r, double2 (&v)[k8Regs], long long base, int tid,
+                                       const double2 *tlo, const double2 *thi) {
+    const bool ph = P.phase_round == r;
+    if (ph) {
+        const long long thr = thr8_offset<F>(P, tid);
+        long long o[k8Regs];
+        reg8_offsets<F>(P, o);
+        double raw[k8Regs];
+#pragma unroll
+        for (int i = 0; i < k8Regs; ++i) raw[i] = global_cost<COST>(P, base + thr + o[i]);
+        if (P.phase_at == 1) {
+#pragma unroll
+            for (int i = 0; i < k8Regs; ++i)
+                v[i] = cmul(v[i], COST == FQ_COST_F64 ? phase_f64(raw[i], P.gamma)
+                                                      : phase_u16((unsigned)raw[i], P, tlo, thi));
+        }
+        if (P.maskA[r]) bfly8<MIX, F>(v, P.A, P.maskA[r]);
+        if (P.phase_at == 2) {
+#pragma unroll
+            for (int i = 0; i < k8Regs; ++i)
+                v[i] = cmul(v[i], COST == FQ_COST_F64 ? phase_f64(raw[i], P.gamma)
+                                                      : phase_u16((unsigned)raw[i], P, tlo, thi));
+        }
+    } else if (P.maskA[r]) {
+        bfly8<MIX, F>(v, P.A, P.maskA[r]);
+    }
+    if (P.maskB[r]) bfly8<MIX, F>(v, P.B, P.maskB[r]);
+}
+
+// NR = 4 (rounds f = 9,0,3,6) or 7 (9,0,3,6 | 6,3,0,9 with round 3 shared: 9,0,3,6,3,0,9)
+template <int MIX, int COST, int NR>
+__global__ void __launch_bounds__(k8Threads, 2) k_pass8(const __grid_constant__ PassParams P) {
+    extern __shared__ double2 smem[];
+    double2 *tile = smem;
+    double2 *tlo = smem + k8Padded;
+    double2 *thi = tlo + kTableLo * kCopies;
+    __shared__ double red[k8Threads / 32];
+    const int tid = threadIdx.x;
+
+    if (COST == FQ_COST_U16 && P.phase_round >= 0 && P.table_hi > 0) {
+        build_phase_tables(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
+        __syncthreads();
+    }
+    double eacc = 0.0;
+    for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+        const long long base = tile_base(P, t);
+        double2 v[k8Regs];
+        {
+            const long long thr = thr8_offset<9>(P, tid);
+            long long o[k8Regs];
+            reg8_offsets<9>(P, o);
+            if (P.init) {
+#pragma unroll
+                for (int i = 0; i < k8Regs; ++i) v[i] = make_double2(P.init_amp, 0.0);
+            } else {
+#pragma unroll
+                for (int i = 0; i < k8Regs; ++i) v[i] = ld_stream(P.psi + base + thr + o[i]);
+            }
+        }
+        round8<MIX, COST, 9>(P, 0, v, base, tid, tlo, thi);
+        t8<9, 0>(tile, v, tid);
+        round8<MIX, COST, 0>(P, 1, v, base, tid, tlo, thi);
+        t8<0, 3>(tile, v, tid);
+        round8<MIX, COST, 3>(P, 2, v, base, tid, tlo, thi);
+        t8<3, 6>(tile, v, tid);
+        round8<MIX, COST, 6>(P, 3, v, base, tid, tlo, thi);
+        if (NR == 7) {
+            t8<6, 3>(tile, v, tid);
+            round8<MIX, COST, 3>(P, 4, v, base, tid, tlo, thi);
+            t8<3, 0>(tile, v, tid);
+            round8<MIX, COST, 0>(P, 5, v, base, tid, tlo, thi);
+            t8<0, 9>(tile, v, tid);
+            round8<MIX, COST, 9>(P, 6, v, base, tid, tlo, thi);
+        }
+        constexpr int FL = (NR == 7) ? 9 : 6;
+        const long long thr = thr8_offset<FL>(P, tid);
+        long long o[k8Regs];
+        reg8_offsets<FL>(P, o);
+        const double fs = P.final_scale;
+#pragma unroll
+        for (int i = 0; i < k8Regs; ++i) {
+            double2 x = v[i];
+            if (MIX == MIX_RX) x = make_double2(x.x * fs, x.y * fs);
+            if (P.expect) eacc += decode_cost<COST>(P, global_cost<COST>(P, base + thr + o[i])) * (x.x * x.x + x.y * x.y);
+            st_stream(P.psi + base + thr + o[i], x);
+        }
+    }
+    if (P.expect) {
+        const double s = block_sum<k8Threads>(eacc, red);
+        if (tid == 0) P.partials[blockIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------- 8-amplitude pass, TMA-staged
+// One persistent 512-thread CTA per SM (16 warps, up to 128 registers).
+// Tile i+1's raw box (and its cost slice) is in flight (cp.async.bulk.tensor)
+// while tile i is transformed; the state stage is re-armed as soon as the last
+// transpose has drained it, the cost stage at the end of the iteration.
+// Results leave with coalesced streaming stores straight from registers.
+template <int COST>
+__host__ __device__ constexpr size_t p8t_smem_bytes(int n_hi) {
+    return 2 * (size_t)k8Padded * 16 + 2 * (size_t)cost_stage_bytes<COST>() +
+           (COST == FQ_COST_U16 ? (size_t)(kTableLo + n_hi) * kCopies * 16 : 0) + 64;
+}
+
+template <int MIX, int COST, int NR>
+__global__ void __launch_bounds__(k8Threads, 1)
+    k_pass8t(const __grid_constant__ PassParams P, const __grid_constant__ CUtensorMap tm_state,
+             const __grid_constant__ CUtensorMap tm_cost) {
+    extern __shared__ __align__(128) double2 sm2[];
+    constexpr int CSTAGE = cost_stage_bytes<COST>() / 16;  // in double2 units
+    double2 *const tlo = sm2 + 2 * k8Padded + 2 * CSTAGE;
+    double2 *const thi = tlo + kTableLo * kCopies;
+    uint64_t *const bar = reinterpret_cast<uint64_t *>(
+        sm2 + 2 * k8Padded + 2 * CSTAGE + (COST == FQ_COST_U16 ? (kTableLo + P.table_hi) * kCopies : 0));
+    // bar[0..1]: state stages, bar[2..3]: cost stages
+    __shared__ double red[k8Threads / 32];
+    const int tid = threadIdx.x;
+
+    const bool need_cost = (P.phase_round >= 0) || P.expect;
+    const bool stage_cost = need_cost && P.cost_tma;
+    const bool load_state = !P.init;
+
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (COST == FQ_COST_U16 && P.phase_round >= 0 && P.table_hi > 0)
+        build_phase_tables(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
+    __syncthreads();
+
+    auto issue_state = [&](long long t, int b) {
+        if (!load_state) return;
+        int c[5];
+        mbar_expect_tx(&bar[b], kStateTxBytes);
+        tile_coords(P.probe_l2 ? (t & 1023) : t, P.tma_rank, P.tma_outer_shift, P.tma_outer_bits, c);
+        tma_load(sm2 + b * k8Padded, &tm_state, P.tma_rank, c, &bar[b]);
+    };
+    auto issue_cost = [&](long long t, int b) {
+        if (!stage_cost) return;
+        int c[5];
+        mbar_expect_tx(&bar[2 + b], cost_stage_bytes<COST>());
+        tile_coords(P.probe_l2 ? (t & 1023) : t, P.cost_rank, P.cost_outer_shift, P.cost_outer_bits, c);
+        tma_load(sm2 + 2 * k8Padded + b * CSTAGE, &tm_cost, P.cost_rank, c, &bar[2 + b]);
+    };
+    if (tid == 0) {
+        for (int k = 0; k < 2; ++k) {
+            const long long t = blockIdx.x + (long long)k * gridDim.x;
+            if (t < P.n_tiles) {
+                issue_state(t, k);
+                issue_cost(t, k);
+            }
+        }
+    }
+
+    double eacc = 0.0;
+    int it = 0;
+    for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x, ++it) {
+        const int b = it & 1;
+        const uint32_t par = (it >> 1) & 1;
+        double2 *const buf = sm2 + b * k8Padded;
+        const void *const cs = sm2 + 2 * k8Padded + b * CSTAGE;
+        const long long base = tile_base(P, t);
+        const long long next = t + 2 * (long long)gridDim.x;
+        bool cost_ready = false;
+        // costs of element i in the round whose register bits start at F
+        auto cost_of = [&](auto ftag, int i) -> double {
+            constexpr int F = decltype(ftag)::value;
+            if (P.cost_tma) {
+                const int e = raw8_base<F>(tid) + raw8_step<F>(i);
+                if (COST == FQ_COST_F64) return static_cast<const double *>(cs)[e];
+                return (double)static_cast<const uint16_t *>(cs)[e];
+            }
+            long long o[k8Regs];
+            reg8_offsets<F>(P, o);
+            return global_cost<COST>(P, base + thr8_offset<F>(P, tid) + o[i]);
+        };
+        auto round = [&](auto ftag, int r, double2 (&v)[k8Regs]) {
+            constexpr int F = decltype(ftag)::value;
+            if (P.phase_round == r) {
+                if (stage_cost && !cost_ready) {
+                    mbar_wait(&bar[2 + b], par);
+                    cost_ready = true;
+                }
+                double raw[k8Regs];
+#pragma unroll
+                for (int i = 0; i < k8Regs; ++i) raw[i] = cost_of(ftag, i);
+                if (P.phase_at == 1) {
+#pragma unroll
+                    for (int i = 0; i < k8Regs; ++i)
+                        v[i] = cmul(v[i], COST == FQ_COST_F64 ? phase_f64(raw[i], P.gamma)
+                                                              : phase_u16((unsigned)raw[i], P, tlo, thi));
+                }
+                if (P.maskA[r]) bfly8<MIX, F>(v, P.A, P.maskA[r]);
+                if (P.phase_at == 2) {
+#pragma unroll
+                    for (int i = 0; i < k8Regs; ++i)
+                        v[i] = cmul(v[i], COST == FQ_COST_F64 ? phase_f64(raw[i], P.gamma)
+                                                              : phase_u16((unsigned)raw[i], P, tlo, thi));
+                }
+            } else if (P.maskA[r]) {
+                bfly8<MIX, F>(v, P.A, P.maskA[r]);
+            }
+            if (P.maskB[r]) bfly8<MIX, F>(v, P.B, P.maskB[r]);
+        };
+
+        double2 v[k8Regs];
+        if (load_state) {
+            mbar_wait(&bar[b], par);
+            const double2 *p = buf + raw8_base<9>(tid);
+#pragma unroll
+            for (int i = 0; i < k8Regs; ++i) v[i] = p[raw8_step<9>(i)];
+        } else {
+#pragma unroll
+            for (int i = 0; i < k8Regs; ++i) v[i] = make_double2(P.init_amp, 0.0);
+        }
+        round(std::integral_constant<int, 9>{}, 0, v);
+        __syncthreads();  // raw box consumed by every thread
+        t8<9, 0>(buf, v, tid);
+        round(std::integral_constant<int, 0>{}, 1, v);
+        t8<0, 3>(buf, v, tid);
+        round(std::integral_constant<int, 3>{}, 2, v);
+        if (NR == 4) {
+            t8_out<3>(buf, v, tid);
+            __syncthreads();
+            t8_in<6>(buf, v, tid);
+            fence_proxy_async();  // order this thread's generic accesses before the TMA refill
+            __syncthreads();
+            if (tid == 0 && next < P.n_tiles) issue_state(next, b);  // state stage drained: re-arm it
+        } else {
+            t8<3, 6>(buf, v, tid);
+        }
+        round(std::integral_constant<int, 6>{}, 3, v);
+        if (NR == 7) {
+            t8<6, 3>(buf, v, tid);
+            round(std::integral_constant<int, 3>{}, 4, v);
+            t8<3, 0>(buf, v, tid);
+            round(std::integral_constant<int, 0>{}, 5, v);
+            t8_out<0>(buf, v, tid);
+            __syncthreads();
+            t8_in<9>(buf, v, tid);
+            fence_proxy_async();
+            __syncthreads();
+            if (tid == 0 && next < P.n_tiles) issue_state(next, b);
+            round(std::integral_constant<int, 9>{}, 6, v);
+        }
+        constexpr int FL = (NR == 7) ? 9 : 6;
+        if (P.expect && stage_cost && !cost_ready) {
+            mbar_wait(&bar[2 + b], par);
+            cost_ready = true;
+        }
+        const long long thr = thr8_offset<FL>(P, tid);
+        long long o[k8Regs];
+        reg8_offsets<FL>(P, o);
+        const double fs = P.final_scale;
+#pragma unroll
+        for (int i = 0; i < k8Regs; ++i) {
+            double2 x = v[i];
+            if (MIX == MIX_RX) x = make_double2(x.x * fs, x.y * fs);
+            if (P.expect) eacc += decode_cost<COST>(P, cost_of(std::integral_constant<int, FL>{}, i)) *
+                                  (x.x * x.x + x.y * x.y);
+            st_stream(P.psi + base + thr + o[i], x);
+        }
+        if (stage_cost) {
+            __syncthreads();  // cost stage b fully read
+            if (tid == 0 && next < P.n_tiles) issue_cost(next, b);
+        }
+    }
+    if (P.expect) {
+        const double s = block_sum<k8Threads>(eacc, red);
         if (tid == 0) P.partials[blockIdx.x] = s;
     }
 }
@@ -416,14 +1181,9 @@ __global__ void __launch_bounds__(kResThreads) k_resident(const __grid_constant_
 // ---------------------------------------------------------------- standalone phase (uint16)
 __global__ void k_phase_u16(double2 *__restrict__ psi, const uint16_t *__restrict__ lv, long long size, double gamma,
                             double scale, double offset) {
-    __shared__ double2 tlo[256], thi[256];
-    build_phase_tables(tlo, thi, gamma, scale, offset);
-    __syncthreads();
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < size;
-         k += (long long)gridDim.x * blockDim.x) {
-        const unsigned v = lv[k];
-        psi[k] = cmul(psi[k], cmul(thi[v >> 8], tlo[v & 255]));
-    }
+         k += (long long)gridDim.x * blockDim.x)
+        psi[k] = cmul(psi[k], phase_f64(decode_u16(lv[k], scale, offset), gamma));
 }
 
 __global__ void k_phase_f64(double2 *__restrict__ psi, const double *__restrict__ costs, long long size,
@@ -498,29 +1258,234 @@ static void rx_coef(double beta, CoefSet &C, double &f) {
     }
 }
 
+// ---- tensor maps (driver entry point fetched through the runtime; no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// Describe one tile (12 physical index bits) of a 2^n vector as a TMA box:
+// runs of tile bits become box dims (full extent), runs of outer bits become
+// box-1 dims whose coordinate comes from the tile number.  `per_amp` elements
+// of `elem_bytes` per amplitude (state: 2 doubles).  False if the layout
+// cannot be expressed (rank > 5, sub-16-B rows or strides).
+static bool build_tile_map(CUtensorMap *map, const void *gaddr, int n, const int *tile_pos, CUtensorMapDataType dt,
+                           int elem_bytes, int per_amp, int &rank, int *outer_shift, int *outer_bits) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    bool is_tile[64] = {};
+    for (int i = 0; i < kTileBits; ++i) is_tile[tile_pos[i]] = true;
+    if (!is_tile[0]) return false;
+    struct Dim { bool tile; int start, len; };
+    std::vector<Dim> dims;
+    const int cap0 = (per_amp == 2) ? 7 : 8;
+    for (int b = 0; b < n;) {
+        int e = b;
+        while (e < n && is_tile[e] == is_tile[b]) ++e;
+        if (is_tile[b]) {
+            int at = b;
+            while (at < e) {
+                const int cap = dims.empty() ? cap0 : 8;
+                const int len = std::min(cap, e - at);
+                dims.push_back({true, at, len});
+                at += len;
+            }
+        } else {
+            dims.push_back({false, b, e - b});
+        }
+        b = e;
+    }
+    if (dims.size() > 5) return false;
+    rank = (int)dims.size();
+    cuuint64_t gdim[5], gstride[5];
+    cuuint32_t box[5], estr[5];
+    int shift = 0;
+    for (int d = 0; d < rank; ++d) {
+        gdim[d] = (cuuint64_t)(d == 0 ? per_amp : 1) << dims[d].len;
+        box[d] = dims[d].tile ? (cuuint32_t)gdim[d] : 1u;
+        estr[d] = 1;
+        if (d > 0) {
+            gstride[d - 1] = ((cuuint64_t)1 << dims[d].start) * per_amp * elem_bytes;
+            if (gstride[d - 1] % 16) return false;
+        }
+        outer_shift[d] = dims[d].tile ? 0 : shift;
+        outer_bits[d] = dims[d].tile ? 0 : dims[d].len;
+        if (!dims[d].tile) shift += dims[d].len;
+    }
+    if ((box[0] * (cuuint32_t)elem_bytes) % 16) return false;
+    for (int d = rank; d < 5; ++d) outer_shift[d] = outer_bits[d] = 0;
+    CUresult r = fn(map, dt, (cuuint32_t)rank, const_cast<void *>(gaddr), gdim, gstride, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 static int max_blocks_per_sm = 2;
 
-template <int MIX, int COST, int NR>
-static int launch_pass(const PassParams &P, int grid, size_t smem, cudaStream_t st) {
+template <int MIX, int COST, int PH, int MA, int MB, int PROBE>
+static int launch_pass16(const PassParams &P, int grid, cudaStream_t st) {
     static bool configured = false;
+    const size_t smem = (size_t)(kTilePadded + (kTableLo + kMaxTableHi) * kCopies) * sizeof(double2);
     if (!configured) {
-        cudaFuncSetAttribute(k_tile_pass<MIX, COST, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kTile + 512) * (int)sizeof(double2));
+        cudaFuncSetAttribute(k_pass16<MIX, COST, PH, MA, MB, PROBE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
         configured = true;
     }
-    k_tile_pass<MIX, COST, NR><<<grid, kThreads, smem, st>>>(P);
-    FQ_LAUNCHED("k_tile_pass");
+    const size_t need = (size_t)(kTilePadded + (kTableLo + P.table_hi) * kCopies) * sizeof(double2);
+    k_pass16<MIX, COST, PH, MA, MB, PROBE><<<grid, kThreads, need, st>>>(P);
+    FQ_LAUNCHED("k_pass16");
     return FQ_OK;
 }
 
-static int dispatch_pass(int mix, int cost, int nr, const PassParams &P, int grid, cudaStream_t st) {
-    const size_t smem = (size_t)(kTile + 512) * sizeof(double2);
-#define FQ_D(M, C, R) if (mix == M && cost == C && nr == R) return launch_pass<M, C, R>(P, grid, smem, st)
-    FQ_D(MIX_RX, FQ_COST_F64, 3); FQ_D(MIX_RX, FQ_COST_F64, 5);
-    FQ_D(MIX_RX, FQ_COST_U16, 3); FQ_D(MIX_RX, FQ_COST_U16, 5);
-    FQ_D(MIX_SU2, FQ_COST_F64, 3); FQ_D(MIX_SU2, FQ_COST_F64, 5);
-    FQ_D(MIX_SU2, FQ_COST_U16, 3); FQ_D(MIX_SU2, FQ_COST_U16, 5);
-#undef FQ_D
+template <int MIX, int COST>
+static int select_pass16(const PassParams &P, int ph, int ma, int mb, int grid, cudaStream_t st) {
+    if (MIX == MIX_SU2) {
+        ma = 0;
+        if (mb != 2) mb = 3;
+    }
+    if (ph != 2 && mb != 2) mb = 3;
+#define FQ_S(PHV, MAV, MBV) \
+    if (ph == PHV && ma == MAV && mb == MBV) return launch_pass16<MIX, COST, PHV, MAV, MBV, 0>(P, grid, st)
+    FQ_S(0, 0, 2); FQ_S(0, 1, 2); FQ_S(0, 0, 3); FQ_S(0, 1, 3);
+    FQ_S(1, 0, 2); FQ_S(1, 1, 2); FQ_S(1, 0, 3); FQ_S(1, 1, 3);
+    if (MIX == MIX_RX) {
+        FQ_S(2, 0, 0); FQ_S(2, 0, 1); FQ_S(2, 1, 0); FQ_S(2, 1, 1);
+    } else {
+        FQ_S(2, 0, 3);
+    }
+#undef FQ_S
+    set_error("select_pass16: unsupported combination ph=%d ma=%d mb=%d", ph, ma, mb);
+    return FQ_ERR_UNSUPPORTED;
+}
+
+template <int MIX, int COST, int NR>
+static int launch_tma(const PassParams &P, const CUtensorMap &ms, const CUtensorMap &mc, int grid, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_pass_tma<MIX, COST, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tma_smem_bytes<COST>(kMaxTableHi));
+        configured = true;
+    }
+    k_pass_tma<MIX, COST, NR><<<grid, kThreads, tma_smem_bytes<COST>(P.table_hi), st>>>(P, ms, mc);
+    FQ_LAUNCHED("k_pass_tma");
+    return FQ_OK;
+}
+
+template <int MIX, int COST, int NR>
+static int launch_pass8(const PassParams &P, int grid, cudaStream_t st) {
+    static bool configured = false;
+    const size_t smem = (size_t)(k8Padded + (kTableLo + kMaxTableHi) * kCopies) * sizeof(double2);
+    if (!configured) {
+        cudaFuncSetAttribute(k_pass8<MIX, COST, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    const size_t need = (size_t)(k8Padded + (kTableLo + P.table_hi) * kCopies) * sizeof(double2);
+    k_pass8<MIX, COST, NR><<<grid, k8Threads, need, st>>>(P);
+    FQ_LAUNCHED("k_pass8");
+    return FQ_OK;
+}
+
+template <int MIX, int COST, int NR>
+static int launch_pass8t(const PassParams &P, const CUtensorMap &ms, const CUtensorMap &mc, int grid,
+                         cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_pass8t<MIX, COST, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)p8t_smem_bytes<COST>(kMaxTableHi));
+        configured = true;
+    }
+    k_pass8t<MIX, COST, NR><<<grid, k8Threads, p8t_smem_bytes<COST>(P.table_hi), st>>>(P, ms, mc);
+    FQ_LAUNCHED("k_pass8t");
+    return FQ_OK;
+}
+
+// 0: 16-amplitude register-load pass, 1: 16-amplitude TMA-staged pass,
+// 2: 8-amplitude register-load pass, 3: 8-amplitude TMA-staged pass
+static int g_kernel = 0;
+static bool g_phase_tables = true;
+static bool g_fuse = true;
+static int g_probe = 0;  // development: time the tile access pattern alone (kernel 0)
+
+// Launches one planned pass with the selected kernel family.  Returns the grid
+// actually used (the expectation partial count) through *grid_out.
+static int dispatch_pass(int mix, int cost, int nr, PassParams &P, long long n_tiles, int n, cudaStream_t st,
+                         int *grid_out) {
+    const int sms = sm_count() > 0 ? sm_count() : 148;
+    alignas(64) CUtensorMap ms, mc;
+    std::memset(&ms, 0, sizeof ms);
+    std::memset(&mc, 0, sizeof mc);
+    P.probe_l2 = g_probe == 2;
+    bool tma = g_kernel == 1 || g_kernel == 3;
+    if (tma)
+        tma = build_tile_map(&ms, P.psi, n, P.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2, P.tma_rank,
+                             P.tma_outer_shift, P.tma_outer_bits);
+    P.cost_tma = 0;
+    if (tma && P.costs && (P.phase_round >= 0 || P.expect)) {
+        const bool ok = (cost == FQ_COST_F64)
+                            ? build_tile_map(&mc, P.costs, n, P.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 1,
+                                             P.cost_rank, P.cost_outer_shift, P.cost_outer_bits)
+                            : build_tile_map(&mc, P.costs, n, P.tile_pos, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, 1,
+                                             P.cost_rank, P.cost_outer_shift, P.cost_outer_bits);
+        P.cost_tma = ok ? 1 : 0;
+    }
+    if (g_kernel == 3 && tma) {
+        const int grid = (int)std::min<long long>(n_tiles, sms);
+        *grid_out = grid;
+#define FQ_8T(M, C, R) if (mix == M && cost == C && nr == R) return launch_pass8t<M, C, R>(P, ms, mc, grid, st)
+        FQ_8T(MIX_RX, FQ_COST_F64, 4); FQ_8T(MIX_RX, FQ_COST_F64, 7);
+        FQ_8T(MIX_RX, FQ_COST_U16, 4); FQ_8T(MIX_RX, FQ_COST_U16, 7);
+        FQ_8T(MIX_SU2, FQ_COST_F64, 4); FQ_8T(MIX_SU2, FQ_COST_F64, 7);
+        FQ_8T(MIX_SU2, FQ_COST_U16, 4); FQ_8T(MIX_SU2, FQ_COST_U16, 7);
+#undef FQ_8T
+    } else if (g_kernel >= 2) {
+        const int grid = (int)std::min<long long>(n_tiles, (long long)sms * 2);
+        *grid_out = grid;
+#define FQ_8(M, C, R) if (mix == M && cost == C && nr == R) return launch_pass8<M, C, R>(P, grid, st)
+        FQ_8(MIX_RX, FQ_COST_F64, 4); FQ_8(MIX_RX, FQ_COST_F64, 7);
+        FQ_8(MIX_RX, FQ_COST_U16, 4); FQ_8(MIX_RX, FQ_COST_U16, 7);
+        FQ_8(MIX_SU2, FQ_COST_F64, 4); FQ_8(MIX_SU2, FQ_COST_F64, 7);
+        FQ_8(MIX_SU2, FQ_COST_U16, 4); FQ_8(MIX_SU2, FQ_COST_U16, 7);
+#undef FQ_8
+    } else if (tma) {
+        const int grid = (int)std::min<long long>(n_tiles, sms);
+        *grid_out = grid;
+#define FQ_T(M, C, R) if (mix == M && cost == C && nr == R) return launch_tma<M, C, R>(P, ms, mc, grid, st)
+        FQ_T(MIX_RX, FQ_COST_F64, 3); FQ_T(MIX_RX, FQ_COST_F64, 5);
+        FQ_T(MIX_RX, FQ_COST_U16, 3); FQ_T(MIX_RX, FQ_COST_U16, 5);
+        FQ_T(MIX_SU2, FQ_COST_F64, 3); FQ_T(MIX_SU2, FQ_COST_F64, 5);
+        FQ_T(MIX_SU2, FQ_COST_U16, 3); FQ_T(MIX_SU2, FQ_COST_U16, 5);
+#undef FQ_T
+    } else {
+        const int grid = (int)std::min<long long>(n_tiles, (long long)sms * max_blocks_per_sm);
+        *grid_out = grid;
+        if (g_probe == 1) {  // memory-pattern ceiling: same tiles, no math, no transposes
+            P.phase_round = -1;
+            P.expect = 0;
+            return launch_pass16<MIX_RX, FQ_COST_U16, 0, 0, 2, 1>(P, grid, st);
+        }
+        if (g_probe == 3 && mix == MIX_RX && cost == FQ_COST_U16 && P.phase_round < 0 &&
+            !(nr == 5 || P.maskB[0] || P.maskB[1] || P.maskB[2])) {  // on-chip compute only
+            P.expect = 0;
+            return P.A.mode ? launch_pass16<MIX_RX, FQ_COST_U16, 0, 1, 2, 2>(P, grid, st)
+                            : launch_pass16<MIX_RX, FQ_COST_U16, 0, 0, 2, 2>(P, grid, st);
+        }
+        const int ph = P.phase_round < 0 ? 0 : (P.phase_at == 1 ? 1 : 2);
+        const bool has_b = nr == 5 || P.maskB[0] || P.maskB[1] || P.maskB[2];
+        const int ma = P.A.mode, mb = has_b ? P.B.mode : 2;
+        if (mix == MIX_RX && cost == FQ_COST_F64) return select_pass16<MIX_RX, FQ_COST_F64>(P, ph, ma, mb, grid, st);
+        if (mix == MIX_RX && cost == FQ_COST_U16) return select_pass16<MIX_RX, FQ_COST_U16>(P, ph, ma, mb, grid, st);
+        if (mix == MIX_SU2 && cost == FQ_COST_F64) return select_pass16<MIX_SU2, FQ_COST_F64>(P, ph, ma, mb, grid, st);
+        if (mix == MIX_SU2 && cost == FQ_COST_U16) return select_pass16<MIX_SU2, FQ_COST_U16>(P, ph, ma, mb, grid, st);
+    }
     set_error("dispatch_pass: unsupported combination");
     return FQ_ERR_UNSUPPORTED;
 }
@@ -578,11 +1543,14 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
     const int n = d->n;
     std::vector<Group> groups;
     std::vector<int> gbase;
-    auto seq = plan_x(n, d->n_layers, d->layers, groups, gbase, true);
+    auto seq = plan_x(n, d->n_layers, d->layers, groups, gbase, g_fuse);
     const int mix = (d->mixer == FQ_MIXER_X) ? MIX_RX : MIX_SU2;
-    const int sms = sm_count() > 0 ? sm_count() : 148;
     const long long n_tiles = 1LL << (n - kTileBits);
-    const int grid = (int)std::min<long long>(n_tiles, (long long)sms * max_blocks_per_sm);
+    int table_hi = 0;
+    if (d->cost_kind == FQ_COST_U16 && d->cost_levels > 0 && g_phase_tables) {
+        const int rows = ((d->cost_levels - 1) >> 6) + 1;
+        table_hi = rows <= kMaxTableHi ? rows : 0;
+    }
     bool init_pending = d->init != 0;
     double2 *psi = static_cast<double2 *>(d->psi);
     const long long size = 1LL << n;
@@ -629,6 +1597,7 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
         P.partials = d->scratch;
         P.init_amp = d->init_amp;
         P.n_tiles = n_tiles;
+        P.table_hi = table_hi;
         for (int i = 0; i < kTileBits; ++i) P.tile_pos[i] = g.tile_pos[i];
         P.init = init_pending ? 1 : 0;
         init_pending = false;
@@ -639,16 +1608,23 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
             if (std::find(g.targets.begin(), g.targets.end(), g.tile_pos[i]) != g.targets.end()) tmask |= 1 << i;
         const bool two = pp.layerB >= 0;
         const bool mid_phase = two && pp.phase_layer >= 0 && pp.phase_at == 2;
-        P.nrounds = mid_phase ? 5 : 3;
-        const int rb[5] = {8, 0, 4, 0, 8};  // first tile bit held in registers per round
-        for (int r = 0; r < 5; ++r) {
-            const int m = (tmask >> rb[r]) & 15;
-            if (P.nrounds == 3) {
-                P.maskA[r] = r < 3 ? m : 0;
-                P.maskB[r] = (r < 3 && two) ? m : 0;
+        // Round programs.  16-amplitude kernels: register tile bits start at
+        // 8,0,4 (| 0,8); 8-amplitude kernel: 9,0,3,6 (| 3,0,9).  Without a phase
+        // between the two layers both sets run back to back in every round.
+        const bool k8 = g_kernel >= 2;
+        const int rb16[5] = {8, 0, 4, 0, 8}, rb8[7] = {9, 0, 3, 6, 3, 0, 9};
+        const int base_rounds = k8 ? 4 : 3;
+        P.nrounds = mid_phase ? 2 * base_rounds - 1 : base_rounds;
+        for (int r = 0; r < 8; ++r) {
+            P.maskA[r] = P.maskB[r] = 0;
+            if (r >= P.nrounds) continue;
+            const int m = k8 ? (tmask >> rb8[r]) & 7 : (tmask >> rb16[r]) & 15;
+            if (!mid_phase) {
+                P.maskA[r] = m;
+                P.maskB[r] = two ? m : 0;
             } else {
-                P.maskA[r] = r < 3 ? m : 0;
-                P.maskB[r] = r >= 2 ? m : 0;
+                P.maskA[r] = r < base_rounds ? m : 0;
+                P.maskB[r] = r >= base_rounds - 1 ? m : 0;
             }
         }
         P.phase_round = -1;
@@ -658,7 +1634,7 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
                 P.phase_round = 0;
                 P.phase_at = 1;
             } else {
-                P.phase_round = 2;
+                P.phase_round = base_rounds - 1;
                 P.phase_at = 2;
             }
         }
@@ -681,7 +1657,8 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
         fill(pp.layerA, P.A);
         if (two) fill(pp.layerB, P.B);
         P.final_scale = fscale;
-        int s = dispatch_pass(mix, d->cost_kind, P.nrounds, P, grid, st);
+        int grid = 0;
+        int s = dispatch_pass(mix, d->cost_kind, P.nrounds, P, n_tiles, n, st, &grid);
         if (s) return s;
         if (P.expect) {
             k_sum_partials<<<1, 32, 0, st>>>(d->scratch, grid, d->expectation_dev);
@@ -845,11 +1822,34 @@ int fq_qaoa_evolve(const fq_evolve_desc *d, void *stream) {
     return run_x_program(d, st);
 }
 
+int fq_set_option(const char *name, int value) {
+    if (!name) return FQ_ERR_ARG;
+    if (std::strcmp(name, "kernel") == 0) {
+        if (value < 0 || value > 3) return FQ_ERR_ARG;
+        g_kernel = value;
+        return FQ_OK;
+    }
+    if (std::strcmp(name, "probe") == 0) {
+        g_probe = value;
+        return FQ_OK;
+    }
+    if (std::strcmp(name, "fuse") == 0) {
+        g_fuse = value != 0;
+        return FQ_OK;
+    }
+    if (std::strcmp(name, "phase_tables") == 0) {
+        g_phase_tables = value != 0;
+        return FQ_OK;
+    }
+    set_error("fq_set_option: unknown option %s", name);
+    return FQ_ERR_ARG;
+}
+
 int fq_plan_x_passes(int n, int n_layers, const fq_layer *layers) {
     if (n <= kTileBits) return n_layers > 0 ? 1 : 0;
     std::vector<Group> groups;
     std::vector<int> gbase;
-    return (int)plan_x(n, n_layers, layers, groups, gbase, true).size();
+    return (int)plan_x(n, n_layers, layers, groups, gbase, g_fuse).size();
 }
 
 int fq_qaoa_evolve_batched(int n, int mixer, const void *costs, int cost_kind, double scale, double offset, int p,

@@ -118,7 +118,7 @@ def _slice_device_costs(dc: DeviceCosts, K: int) -> list[DeviceCosts]:
     for r in range(K):
         f = dc.f64[r * size:(r + 1) * size] if dc.f64 is not None else None
         u = dc.u16[r * size:(r + 1) * size] if dc.u16 is not None else None
-        out.append(DeviceCosts(n_local, f64=f, u16=u, scale=dc.scale, offset=dc.offset))
+        out.append(DeviceCosts(n_local, f64=f, u16=u, scale=dc.scale, offset=dc.offset, levels=dc.levels))
     return out
 
 

@@ -94,6 +94,7 @@ def run_program(psi, n: int, mixer: str, layers: Sequence[tuple], dc=None, su2: 
     if dc is not None:
         kind, cp, scale, offset = dc.kernel_view()
         desc.cost_kind, desc.costs, desc.cost_scale, desc.cost_offset = kind, cp, scale, offset
+        desc.cost_levels = dc.levels if kind == _lib.COST_U16 else 0
     desc.mixer = _lib.MIXER_CODES[mixer]
     desc.n_layers = len(layers)
     desc.layers = arr
