@@ -186,8 +186,21 @@ int fq_qaoa_evolve_batched(int n, int mixer, const void *costs, int cost_kind, d
  * byte model in bench.py / DESIGN.md). */
 int fq_plan_x_passes(int n, int n_layers, const fq_layer *layers);
 
-/* Runtime switches (testing / A-B measurement): "tma" = 1 (default) stages
- * tiles with cp.async.bulk.tensor, 0 forces the register-load pass kernel. */
+/* Passes of the last tiled X/custom program run on this host thread's
+ * process: returns the pass count; for i < max fills info[5*i..5*i+4] =
+ * (round program: 0 = 8|0|4, 1 = 8|4, 2 = 8|0|4|0|8, 3 = 8|4|8, -1 = standalone
+ * phase; phase mode; target count; generates |+>; accumulates the expectation)
+ * and, with option "time_passes" on, ms[i] = CUDA-event time of pass i on the
+ * launching stream (synchronises with the program's last event).  NULL
+ * arrays are skipped. */
+int fq_last_passes(int *info, float *ms, int max);
+
+/* Runtime switches (testing / A-B measurement):
+ *   "prefetch"     L2 bulk-prefetch distance of the pass kernel in grid strides (default 1, 0 = off)
+ *   "fuse"         fuse the passes at layer boundaries (default 1)
+ *   "phase_tables" uint16 phase through shared-memory tables (default 1, 0 = sincos)
+ *   "plan"         group plan: -1 cost model (default), 0 legacy, 1 small fusion groups
+ *   "time_passes"  record a CUDA event after every pass (read with fq_last_passes) */
 int fq_set_option(const char *name, int value);
 
 #ifdef __cplusplus

@@ -16,7 +16,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libfqaoa.so")
-SOURCES = ["ops.cu", "evolve.cu"]
+SOURCES = ["ops.cu", "evolve.cu", "pass_rx_u16_light.cu", "pass_rx_u16_heavy.cu", "pass_rx_f64_light.cu",
+           "pass_rx_f64_heavy.cu", "pass_su2.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -35,33 +36,63 @@ def host_compiler() -> list[str]:
     return []
 
 
+def _headers() -> list[str]:
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + \
+        [os.path.join(INCLUDE, "fqaoa.h"), __file__]
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INCLUDE, "fqaoa.h"), __file__]
+    deps = [os.path.join(CSRC, f) for f in SOURCES] + _headers()
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
+    """Compile every translation unit (in parallel; an object is rebuilt when
+    its source or any header is newer) and link libfqaoa.so."""
     if not force and not _stale():
         return LIB
-    objs = []
     tmpdir = os.path.join(HERE, "build")
     os.makedirs(tmpdir, exist_ok=True)
     common = [nvcc(), *host_compiler(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", INCLUDE, "-I", CSRC, "--expt-relaxed-constexpr"]
     if verbose:
         common += ["-Xptxas", "-v"]
+    hdr_t = max(os.path.getmtime(h) for h in _headers())
+    objs, procs = [], []
     for src in SOURCES:
+        path = os.path.join(CSRC, src)
         obj = os.path.join(tmpdir, src.replace(".cu", ".o"))
-        cmd = [*common, "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0 or verbose:
-            sys.stderr.write(r.stdout + r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(path)):
+            continue
+        procs.append((src, [*common, "-c", path, "-o", obj]))
+    jobs = jobs or max(1, min(len(procs), os.cpu_count() or 1))
+    running: list = []
+    failed = []
+
+    def reap(block: bool) -> None:
+        for item in list(running):
+            src, p = item
+            if block or p.poll() is not None:
+                out, err = p.communicate()
+                if p.returncode != 0 or verbose:
+                    sys.stderr.write(out + err)
+                if p.returncode != 0:
+                    failed.append(src)
+                running.remove(item)
+
+    for src, cmd in procs:
+        while len(running) >= jobs:
+            reap(False)
+            if len(running) >= jobs:
+                running[0][1].wait()
+        running.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    reap(True)
+    if failed:
+        raise RuntimeError(f"nvcc failed on {', '.join(failed)}")
     tmp_lib = LIB + ".tmp"
     cmd = [nvcc(), *host_compiler(), *ARCH, "-shared", "-o", tmp_lib, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -57,6 +57,7 @@ _SIGS = {
     "fq_qaoa_evolve_batched": ([I, I, P, I, D, D, I, I, P, P, P, P, P, P], I),
     "fq_plan_x_passes": ([I, I, ctypes.POINTER(FqLayer)], I),
     "fq_set_option": ([ctypes.c_char_p, I], I),
+    "fq_last_passes": ([P, P, I], I),
 }
 
 EXPORTED = tuple(_SIGS)

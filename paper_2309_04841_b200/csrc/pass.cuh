@@ -1,0 +1,484 @@
+// Tiled pass kernel of the fused QAOA evolution (sm_100a), shared by the
+// evolve.cu planner and the per-(mixer, cost) instantiation units
+// pass_*.cu, which are compiled in parallel.
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <type_traits>
+#include <vector>
+
+#include "common.cuh"
+
+namespace fq {
+
+
+constexpr int kTileBits = 12;
+constexpr int kTile = 1 << kTileBits;
+constexpr int kThreads = 256;
+constexpr int kRegs = 16;
+
+enum { MIX_RX = 0, MIX_SU2 = 1 };
+enum { PAT8 = 0, PAT0 = 1, PAT4 = 2 };  // tile bits held in registers: 8-11 / 0-3 / 4-7
+
+// Round programs (register patterns visited by one pass):
+//   SEQ_840   8 | 0 | 4        one layer (or two with no phase between) on a 12-bit group
+//   SEQ_84    8 | 4            same, targets only in tile bits 4-11
+//   SEQ_84048 8 | 0 | 4 ph 4 | 0 | 8   two layers with the phase between, 12-bit group
+//   SEQ_848   8 | 4 ph 4 | 8            two layers with the phase between, targets in bits 4-11
+enum { SEQ_840 = 0, SEQ_84 = 1, SEQ_84048 = 2, SEQ_848 = 3 };
+
+__host__ __device__ constexpr int seq_rounds(int seq) {
+    return seq == SEQ_840 ? 3 : seq == SEQ_84 ? 2 : seq == SEQ_84048 ? 5 : 3;
+}
+__host__ __device__ constexpr int seq_pat(int seq, int r) {
+    return seq == SEQ_840   ? (r == 0 ? PAT8 : r == 1 ? PAT0 : PAT4)
+         : seq == SEQ_84    ? (r == 0 ? PAT8 : PAT4)
+         : seq == SEQ_84048 ? (r == 0 || r == 4 ? PAT8 : (r == 1 || r == 3) ? PAT0 : PAT4)
+                            : (r == 1 ? PAT4 : PAT8);
+}
+__host__ __device__ constexpr int pat_first_bit(int pat) { return pat == PAT8 ? 8 : pat == PAT0 ? 0 : 4; }
+__host__ __device__ constexpr bool seq_heavy(int seq) { return seq == SEQ_84048 || seq == SEQ_848; }
+
+struct CoefSet {
+    double r;      // RX: t (mode 0) or u (mode 1)
+    int mode;      // RX: 0 -> (1, t), 1 -> (u, 1)
+    double2 a[kTileBits], b[kTileBits];  // SU2: per tile bit
+};
+
+struct PassParams {
+    double2 *psi;
+    const void *costs;
+    double cost_scale, cost_offset;
+    double *partials;
+    double init_amp;
+    double gamma;
+    double final_scale;
+    long long n_tiles;
+    int tile_pos[kTileBits];  // physical bit of tile bit i (ascending)
+    int init;                 // generate |+> instead of loading
+    int expect;               // accumulate sum c|x|^2 in the last round
+    int table_hi;             // U16 phase: rows of the high table (0 -> sincos of the decoded cost)
+    unsigned char maskA[8], maskB[8];  // per round: register bits getting set A / set B butterflies
+    int pf_dist;              // L2 prefetch distance in grid strides (0: off)
+    int run_bits;             // tile bits 0..run_bits-1 sit at physical bits 0..run_bits-1 (contiguous runs)
+    int pf_cost;              // also prefetch the cost slice of the tile
+    int probe;                // development: 1 no cost loads, 2 fixed table row, 4 no phase multiply
+    long long roff[3][kRegs]; // per pattern: physical offset of register i (read from the constant bank,
+                              // so no register holds the 16 offsets across the rounds)
+    CoefSet A, B;
+};
+
+constexpr int kTableLo = 64;     // low-table rows (6 level bits)
+constexpr int kMaxTableHi = 256; // high-table rows -> levels < 16384 use tables
+constexpr int kCopies = 8;       // one copy per 16-B bank group: conflict-free random lookups
+
+template <int PAT>
+__device__ __forceinline__ int tile_bit_of_reg(int j) {
+    return PAT == PAT8 ? 8 + j : (PAT == PAT0 ? j : 4 + j);
+}
+
+// Transpose scratch layout: tile index e lives at slot e + (e >> 4) (one pad
+// entry per 16).  For all three register patterns the thread part and the
+// register part of the slot are additive (slot = pat_base(tid) + pat_step(i)),
+// so every access is [base register + immediate], and a quarter-warp's eight
+// 16-B accesses always fall in eight distinct bank groups.
+constexpr int kTilePadded = kTile + kTile / 16;
+
+template <int PAT>
+__device__ __forceinline__ int pat_base(int tid) {
+    if (PAT == PAT8) return tid + (tid >> 4);
+    if (PAT == PAT0) return 17 * tid;
+    return (tid & 15) + 272 * (tid >> 4);
+}
+template <int PAT>
+__host__ __device__ constexpr int pat_step(int i) {
+    return PAT == PAT8 ? 272 * i : (PAT == PAT0 ? i : 17 * i);
+}
+
+// physical offset of this thread's element 0 for pattern PAT
+template <int PAT>
+__device__ __forceinline__ long long thread_offset(const PassParams &P, int tid) {
+    long long off = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        int tb;
+        if (PAT == PAT8) tb = j;
+        else if (PAT == PAT0) tb = 4 + j;
+        else tb = (j < 4) ? j : j + 4;
+        if ((tid >> j) & 1) off += 1LL << P.tile_pos[tb];
+    }
+    return off;
+}
+
+template <int FROM, int TO>
+__device__ __forceinline__ void transpose(double2 *sm, double2 (&v)[kRegs], int tid) {
+    double2 *p = sm + pat_base<FROM>(tid);
+#pragma unroll
+    for (int i = 0; i < kRegs; ++i) p[pat_step<FROM>(i)] = v[i];
+    __syncthreads();
+    const double2 *q = sm + pat_base<TO>(tid);
+#pragma unroll
+    for (int i = 0; i < kRegs; ++i) v[i] = q[pat_step<TO>(i)];
+    __syncthreads();
+}
+
+// ---- butterflies
+__device__ __forceinline__ void bfly_rx0(double2 &x0, double2 &x1, double t) {
+    // (x0 - i t x1, x1 - i t x0)
+    const double2 a = x0, b = x1;
+    x0 = make_double2(fma(t, b.y, a.x), fma(-t, b.x, a.y));
+    x1 = make_double2(fma(t, a.y, b.x), fma(-t, a.x, b.y));
+}
+__device__ __forceinline__ void bfly_rx1(double2 &x0, double2 &x1, double u) {
+    // (u x0 - i x1, u x1 - i x0)
+    const double2 a = x0, b = x1;
+    x0 = make_double2(fma(u, a.x, b.y), fma(u, a.y, -b.x));
+    x1 = make_double2(fma(u, b.x, a.y), fma(u, b.y, -a.x));
+}
+__device__ __forceinline__ void bfly_su2(double2 &x0, double2 &x1, double2 a, double2 b) {
+    // y0 = a x0 - conj(b) x1 ; y1 = b x0 + conj(a) x1   (reference _kernels.py:26-27)
+    const double2 p = x0, q = x1;
+    x0 = make_double2(a.x * p.x - a.y * p.y - b.x * q.x - b.y * q.y,
+                      a.x * p.y + a.y * p.x - b.x * q.y + b.y * q.x);
+    x1 = make_double2(b.x * p.x - b.y * p.y + a.x * q.x + a.y * q.y,
+                      b.x * p.y + b.y * p.x + a.x * q.y - a.y * q.x);
+}
+
+// Butterflies of one coefficient set on the register bits in `mask`.
+// M: RX form 0 -> (1, t), 1 -> (u, 1), 3 -> chosen at run time.
+template <int MIX, int M, int PAT>
+__device__ __forceinline__ void bfly16(double2 (&v)[kRegs], const CoefSet &C, int mask) {
+    if (MIX == MIX_RX && M == 3) {
+        if (C.mode == 0) bfly16<MIX, 0, PAT>(v, C, mask);
+        else bfly16<MIX, 1, PAT>(v, C, mask);
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (!((mask >> j) & 1)) continue;
+        if (MIX == MIX_RX) {
+            const double r = C.r;
+            if (M == 0) {
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i)
+                    if (!(i & (1 << j))) bfly_rx0(v[i], v[i | (1 << j)], r);
+            } else {
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i)
+                    if (!(i & (1 << j))) bfly_rx1(v[i], v[i | (1 << j)], r);
+            }
+        } else {
+            const int tb = tile_bit_of_reg<PAT>(j);
+            const double2 a = C.a[tb], b = C.b[tb];
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i)
+                if (!(i & (1 << j))) bfly_su2(v[i], v[i | (1 << j)], a, b);
+        }
+    }
+}
+
+// ---- phase
+// exp(-i gamma c) for a float64 cost: the reference's angle = gamma * c, then sincos.
+__device__ __forceinline__ double2 phase_f64(double c, double gamma) {
+    double s, co;
+    sincos(gamma * c, &s, &co);
+    return make_double2(co, -s);
+}
+
+static __device__ __noinline__ double2 phase_sincos_u16(unsigned v, double scale, double offset, double gamma) {
+    return phase_f64(decode_u16((uint16_t)v, scale, offset), gamma);
+}
+
+// raw cost entry as held in registers: the double itself, or the uint16 level
+template <int COST>
+using CostRaw = typename std::conditional<COST == FQ_COST_F64, double, unsigned>::type;
+
+template <int COST>
+__device__ __forceinline__ CostRaw<COST> load_cost(const PassParams &P, long long k) {
+    if constexpr (COST == FQ_COST_F64) return __ldcs(static_cast<const double *>(P.costs) + k);
+    else return (unsigned)__ldcs(static_cast<const unsigned short *>(P.costs) + k);
+}
+
+template <int COST>
+__device__ __forceinline__ double decode_cost(const PassParams &P, CostRaw<COST> raw) {
+    if constexpr (COST == FQ_COST_F64) return raw;
+    else return decode_u16((uint16_t)raw, P.cost_scale, P.cost_offset);
+}
+
+// exp(-i gamma c): float64 -> sincos; uint16 level v -> T_hi[v >> 6] * T_lo[v & 63],
+// each table replicated once per 16-B bank group (copy = lane & 7) so a
+// quarter-warp's random lookups never conflict.
+template <int COST>
+__device__ __forceinline__ double2 phase16(const PassParams &P, CostRaw<COST> raw, const double2 *tlo,
+                                           const double2 *thi) {
+    if constexpr (COST == FQ_COST_F64) {
+        return phase_f64(raw, P.gamma);
+    } else {
+        if (P.table_hi == 0) return phase_sincos_u16(raw, P.cost_scale, P.cost_offset, P.gamma);
+        const int cp = threadIdx.x & (kCopies - 1);
+        return cmul(thi[(raw >> 6) * kCopies + cp], tlo[(raw & 63) * kCopies + cp]);
+    }
+}
+
+// e^{-i gamma c} tables for uint16 levels: c = scale*(64 h + l) + offset
+__device__ __forceinline__ void build_phase_tables(double2 *tlo, double2 *thi, int n_hi, double gamma, double scale,
+                                                   double offset) {
+    for (int i = threadIdx.x; i < kTableLo + n_hi; i += blockDim.x) {
+        double s, c;
+        if (i < kTableLo) sincos(gamma * (scale * (double)i), &s, &c);
+        else sincos(gamma * (scale * (double)(64 * (i - kTableLo)) + offset), &s, &c);
+        double2 *row = (i < kTableLo) ? tlo + i * kCopies : thi + (i - kTableLo) * kCopies;
+#pragma unroll
+        for (int k = 0; k < kCopies; ++k) row[k] = make_double2(c, -s);
+    }
+}
+
+// tile number -> base address: insert a zero at every tile bit position
+__device__ __forceinline__ long long tile_base(const PassParams &P, long long t) {
+    long long base = t;
+#pragma unroll
+    for (int j = 0; j < kTileBits; ++j) {
+        const int p = P.tile_pos[j];
+        base = ((base >> p) << (p + 1)) | (base & ((1LL << p) - 1));
+    }
+    return base;
+}
+
+// L2 prefetch of a future tile: the tile is 2^(12-s) contiguous runs of 2^s
+// amplitudes (s = P.run_bits); one cp.async.bulk.prefetch per run, spread
+// over the CTA's threads, so the tile's loads later hit L2.
+__device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int COST>
+__device__ __forceinline__ void prefetch_tile(const PassParams &P, long long t, bool state) {
+    const int s = P.run_bits;
+    const int runs = 1 << (kTileBits - s);
+    const long long base = tile_base(P, t);
+    constexpr int cb = COST == FQ_COST_F64 ? 8 : 2;
+    const int cbytes = cb << s;
+    for (int r = threadIdx.x; r < runs; r += blockDim.x) {
+        long long off = base;
+#pragma unroll 1
+        for (int j = 0; j < kTileBits - s; ++j)
+            if ((r >> j) & 1) off += 1LL << P.tile_pos[s + j];
+        if (state) bulk_prefetch_l2(P.psi + off, 16u << s);
+        if (P.pf_cost && (cbytes & 15) == 0)
+            bulk_prefetch_l2(static_cast<const char *>(P.costs) + off * cb, (uint32_t)cbytes);
+    }
+}
+
+// Target mask of round r.  K = 0: the run-time masks of PassParams; K = 4: every
+// visited quad is all targets; K = 1..3 (SEQ_84 / SEQ_848 only): the PAT8 quad is
+// all targets and the PAT4 quad has its top K bits as targets (a high group of
+// 4 + K targets above 8 - K spectators).
+enum { K_RUNTIME = 0, K_FULL = 4 };
+template <int K, int SEQ>
+__device__ __forceinline__ int round_mask(const unsigned char *rt, int r) {
+    if constexpr (K == K_RUNTIME) return rt[r];
+    else if constexpr (K == K_FULL) return 0xF;
+    else return seq_pat(SEQ, r) == PAT4 ? ((0xF << (4 - K)) & 0xF) : 0xF;
+}
+
+// ---------------------------------------------------------------- the pass kernel
+// Register-load pass, 256 threads x 16 amplitudes per 2^12 tile, 2 CTAs/SM
+// (grid-stride over tiles).  Everything that varies between passes of one
+// program is a template parameter, so the tile loop has no runtime branches
+// on it:
+//   SEQ: round program (see SEQ_*);
+//   PH: 0 no phase, 1 phase before set A in round 0, 2 phase between set A and
+//       set B in the middle (PAT4) round of a heavy SEQ;
+//   MA, MB: RX form of sets A/B (0: (1, tan b), 1: (cot b, 1), 3: chosen at run
+//       time); MB = 2: no set B;
+//   K: target-mask class of the rounds (see round_mask): compile-time masks keep
+//       the butterfly code branch-free (run-time masks force register moves at
+//       every merge point).
+template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K>
+__global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ PassParams P) {
+    extern __shared__ double2 smem[];
+    double2 *tile = smem;
+    double2 *tlo = smem + kTilePadded;
+    double2 *thi = tlo + kTableLo * kCopies;
+    __shared__ double red[kThreads / 32];
+    const int tid = threadIdx.x;
+    constexpr bool HAS_B = MB != 2;
+    constexpr bool HEAVY = seq_heavy(SEQ);
+    static_assert(!HEAVY || (PH == 2 && HAS_B), "heavy round programs carry the mid-layer phase");
+    static_assert(HEAVY || PH != 2, "the mid-layer phase needs a heavy round program");
+    constexpr int NR = seq_rounds(SEQ);
+    constexpr int LAST = seq_pat(SEQ, NR - 1);
+
+    if (COST == FQ_COST_U16 && PH != 0) {
+        if (P.table_hi > 0) build_phase_tables(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
+        __syncthreads();
+    }
+    const long long thr8 = thread_offset<PAT8>(P, tid);
+    const long long thr4 = thread_offset<PAT4>(P, tid);
+    const long long thrL = LAST == PAT8 ? thr8 : thr4;
+    double eacc = 0.0;
+
+    if (P.pf_dist > 1) {  // prologue: tiles 1 .. pf_dist-1 of this CTA
+        for (int d = 1; d < P.pf_dist; ++d) {
+            const long long tp = blockIdx.x + (long long)d * gridDim.x;
+            if (tp < P.n_tiles) prefetch_tile<COST>(P, tp, !P.init);
+        }
+    }
+    for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+        const long long base = tile_base(P, t);
+        if (P.pf_dist > 0) {
+            const long long tp = t + (long long)P.pf_dist * gridDim.x;
+            if (tp < P.n_tiles) prefetch_tile<COST>(P, tp, !P.init);
+        }
+        double2 v[kRegs];
+        CostRaw<COST> raw[kRegs];  // cost entries of the phase round, loaded with the state
+        {
+            const long long *o = P.roff[PAT8];
+            if (P.init) {
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) v[i] = make_double2(P.init_amp, 0.0);
+            } else {
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) v[i] = ld_stream(P.psi + base + thr8 + o[i]);
+            }
+            if (PH == 1) {
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost<COST>(P, base + thr8 + o[i]);
+            }
+        }
+        if (PH == 2) {
+            const long long *o = P.roff[PAT4];
+            if (P.probe & 1) {
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) raw[i] = (CostRaw<COST>)((tid * 7 + i * 131) & 1023);
+            } else {
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost<COST>(P, base + thr4 + o[i]);
+            }
+        }
+        auto phase_all = [&]() {
+            // keep the table lookups behind the preceding butterflies: hoisted
+            // early they would hold 64 registers of phase factors and spill
+            asm volatile("" ::: "memory");
+            if (P.probe & 4) return;
+            if (P.probe & 2) {
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase16<COST>(P, (CostRaw<COST>)0, tlo, thi));
+                return;
+            }
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase16<COST>(P, raw[i], tlo, thi));
+        };
+        // ---- round 0 (PAT8)
+        if (PH == 1) phase_all();
+        bfly16<MIX, MA, PAT8>(v, P.A, round_mask<K, SEQ>(P.maskA, 0));
+        if constexpr (SEQ == SEQ_840) {
+            if (HAS_B) bfly16<MIX, MB, PAT8>(v, P.B, round_mask<K, SEQ>(P.maskB, 0));
+            transpose<PAT8, PAT0>(tile, v, tid);
+            bfly16<MIX, MA, PAT0>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+            if (HAS_B) bfly16<MIX, MB, PAT0>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
+            transpose<PAT0, PAT4>(tile, v, tid);
+            bfly16<MIX, MA, PAT4>(v, P.A, round_mask<K, SEQ>(P.maskA, 2));
+            if (HAS_B) bfly16<MIX, MB, PAT4>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
+        } else if constexpr (SEQ == SEQ_84) {
+            if (HAS_B) bfly16<MIX, MB, PAT8>(v, P.B, round_mask<K, SEQ>(P.maskB, 0));
+            transpose<PAT8, PAT4>(tile, v, tid);
+            bfly16<MIX, MA, PAT4>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+            if (HAS_B) bfly16<MIX, MB, PAT4>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
+        } else if constexpr (SEQ == SEQ_84048) {
+            transpose<PAT8, PAT0>(tile, v, tid);
+            bfly16<MIX, MA, PAT0>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+            transpose<PAT0, PAT4>(tile, v, tid);
+            bfly16<MIX, MA, PAT4>(v, P.A, round_mask<K, SEQ>(P.maskA, 2));
+            phase_all();
+            bfly16<MIX, MB, PAT4>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
+            transpose<PAT4, PAT0>(tile, v, tid);
+            bfly16<MIX, MB, PAT0>(v, P.B, round_mask<K, SEQ>(P.maskB, 3));
+            transpose<PAT0, PAT8>(tile, v, tid);
+            bfly16<MIX, MB, PAT8>(v, P.B, round_mask<K, SEQ>(P.maskB, 4));
+        } else {  // SEQ_848
+            transpose<PAT8, PAT4>(tile, v, tid);
+            bfly16<MIX, MA, PAT4>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+            phase_all();
+            bfly16<MIX, MB, PAT4>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
+            transpose<PAT4, PAT8>(tile, v, tid);
+            bfly16<MIX, MB, PAT8>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
+        }
+        // ---- store (+ expectation) in the last round's pattern
+        const long long *o = P.roff[LAST];
+        const double fs = P.final_scale;
+        if (P.expect) {  // cost entries of the last pattern (only the program's final pass)
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i) raw[i] = load_cost<COST>(P, base + thrL + o[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < kRegs; ++i) {
+            double2 x = v[i];
+            if (MIX == MIX_RX) x = make_double2(x.x * fs, x.y * fs);
+            if (P.expect) eacc += decode_cost<COST>(P, raw[i]) * (x.x * x.x + x.y * x.y);
+            st_stream(P.psi + base + thrL + o[i], x);
+        }
+    }
+    if (P.expect) {
+        const double s = block_sum<kThreads>(eacc, red);
+        if (tid == 0) P.partials[blockIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------- launch
+template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K>
+static int launch_pass16(const PassParams &P, int grid, cudaStream_t st) {
+    static bool configured = false;
+    const size_t smem = (size_t)(kTilePadded + (kTableLo + kMaxTableHi) * kCopies) * sizeof(double2);
+    if (!configured) {
+        cudaFuncSetAttribute(k_pass16<MIX, COST, SEQ, PH, MA, MB, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        configured = true;
+    }
+    const size_t need = (size_t)(kTilePadded + (kTableLo + P.table_hi) * kCopies) * sizeof(double2);
+    k_pass16<MIX, COST, SEQ, PH, MA, MB, K><<<grid, kThreads, need, st>>>(P);
+    FQ_LAUNCHED("k_pass16");
+    return FQ_OK;
+}
+
+// Template dispatch for one round program SEQ of one (mixer, cost) pair.
+// ph/ma/mb/k as the k_pass16 parameters (ma/mb already normalised by the
+// caller); a mask class k without an instantiation runs with the run-time
+// masks (K_RUNTIME), which PassParams always carries.
+template <int MIX, int COST, int SEQ>
+static int select_seq(const PassParams &P, int ph, int ma, int mb, int k, int grid, cudaStream_t st) {
+    constexpr bool kHigh = SEQ == SEQ_84 || SEQ == SEQ_848;
+#define FQ_K(PHV, MAV, MBV)                                                                                  \
+    if (ph == PHV && ma == MAV && mb == MBV) {                                                               \
+        if (k == K_FULL) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_FULL>(P, grid, st);          \
+        if constexpr (kHigh && MIX == MIX_RX) {                                                              \
+            if (k == 1) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 1>(P, grid, st);                \
+            if (k == 2) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 2>(P, grid, st);                \
+            if (k == 3) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 3>(P, grid, st);                \
+        }                                                                                                    \
+        return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_RUNTIME>(P, grid, st);                        \
+    }
+    if constexpr (seq_heavy(SEQ)) {
+        if constexpr (MIX == MIX_RX) {
+            FQ_K(2, 0, 0) FQ_K(2, 0, 1) FQ_K(2, 1, 0) FQ_K(2, 1, 1)
+        } else {
+            FQ_K(2, 0, 3)
+        }
+    } else {
+        FQ_K(0, 0, 2) FQ_K(0, 0, 3) FQ_K(1, 0, 2) FQ_K(1, 0, 3)
+        if constexpr (MIX == MIX_RX) { FQ_K(0, 1, 2) FQ_K(0, 1, 3) FQ_K(1, 1, 2) FQ_K(1, 1, 3) }
+    }
+#undef FQ_K
+    set_error("k_pass16: no instantiation for seq=%d ph=%d ma=%d mb=%d", SEQ, ph, ma, mb);
+    return FQ_ERR_UNSUPPORTED;
+}
+
+// Instantiation units (pass_*.cu), compiled in parallel.
+int launch_pass_rx_u16_light(const PassParams &P, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
+int launch_pass_rx_u16_heavy(const PassParams &P, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
+int launch_pass_rx_f64_light(const PassParams &P, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
+int launch_pass_rx_f64_heavy(const PassParams &P, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
+int launch_pass_su2(const PassParams &P, int cost, int seq, int ph, int mb, int k, int grid, cudaStream_t st);
+
+}  // namespace fq

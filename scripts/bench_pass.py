@@ -4,6 +4,7 @@ Times the fused LABS program at n (default 26) under each option combination
 and prints ms/step, ms/pass and effective GB/s of the pass stream."""
 
 import argparse
+import ctypes
 import itertools
 import json
 import math
@@ -23,7 +24,8 @@ def main():
     ap.add_argument("--n", type=int, default=26)
     ap.add_argument("--p", type=int, default=10)
     ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--opts", default="kernel=2,0,1;phase_tables=1,0")
+    ap.add_argument("--opts", default="plan=0,1")
+    ap.add_argument("--detail", action="store_true", help="per-pass CUDA-event times of one step")
     args = ap.parse_args()
     n, p = args.n, args.p
     sim = QaoaSimulator(terms=labs_terms(n))
@@ -60,6 +62,19 @@ def main():
             print(json.dumps({"opts": dict(zip(names, combo)), "mode": label, "ms_step": round(ms, 3),
                               "passes": passes, "ms_pass": round(ms / passes, 4),
                               "GBps": round(byts / ms / 1e6, 1), "E": float(e.item())}), flush=True)
+            if args.detail:
+                _lib.call("fq_set_option", b"time_passes", 1)
+                fn()
+                info = (ctypes.c_int * (5 * 64))()
+                tms = (ctypes.c_float * 64)()
+                cnt = _lib.load().fq_last_passes(info, tms, 64)
+                _lib.call("fq_set_option", b"time_passes", 0)
+                names_seq = {-1: "phase", 0: "8|0|4", 1: "8|4", 2: "8|0|4|0|8", 3: "8|4|8"}
+                for i in range(cnt):
+                    sq, ph, nt, ini, ex = info[5 * i:5 * i + 5]
+                    nb = (0 if ini else S) + S + (C if (ph or ex) else 0)
+                    print(f"    pass {i:2d} {names_seq[sq]:10s} ph={ph} targets={nt:2d} init={ini} exp={ex} "
+                          f"{tms[i]:.4f} ms {nb / tms[i] / 1e6:7.1f} GB/s", flush=True)
     for nm in names:
         _lib.call("fq_set_option", nm.encode(), 1)
 

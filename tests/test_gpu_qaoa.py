@@ -41,19 +41,19 @@ def test_matches_reference_golden(golden, case):
     assert sim.get_overlap(res) == pytest.approx(float(golden[f"sim/{case}/overlap"]), abs=1e-10)
 
 
-@pytest.fixture(params=[3, 2, 1, 0], ids=["pass8t", "pass8", "tma16", "ldg16"])
-def pass_kernel(request):
-    """Run a test with each tiled pass kernel family (default: pass8)."""
+@pytest.fixture(params=[-1, 0, 1], ids=["plan-auto", "plan-legacy", "plan-smallfuse"])
+def pass_plan(request):
+    """Run a test under each group plan of the tiled pass program."""
     from paper_2309_04841_b200 import _lib
 
-    _lib.call("fq_set_option", b"kernel", request.param)
+    _lib.call("fq_set_option", b"plan", request.param)
     yield request.param
-    _lib.call("fq_set_option", b"kernel", 2)
+    _lib.call("fq_set_option", b"plan", -1)
 
 
 @pytest.mark.parametrize("n,p,seed", [(13, 1, 0), (13, 3, 1), (14, 2, 2), (16, 4, 3), (17, 5, 4), (19, 3, 5),
                                       (22, 2, 6), (24, 2, 7), (25, 1, 8)])
-def test_tiled_x_labs_vs_oracle(n, p, seed, pass_kernel):
+def test_tiled_x_labs_vs_oracle(n, p, seed, pass_plan):
     """Fused tiled passes (uint16 phase tables, alternating-order layer fusion)."""
     rng = np.random.default_rng(seed)
     g, b = rng.uniform(-1, 1, p), rng.uniform(-1.6, 1.6, p)
@@ -72,7 +72,7 @@ def test_tiled_x_labs_vs_oracle(n, p, seed, pass_kernel):
 
 
 @pytest.mark.parametrize("n,p,seed", [(13, 2, 10), (15, 3, 11), (18, 2, 12)])
-def test_tiled_x_float_costs_vs_oracle(n, p, seed, pass_kernel):
+def test_tiled_x_float_costs_vs_oracle(n, p, seed, pass_plan):
     """Float-weight diagonal: float64 cost path with sincos in the pass."""
     rng = np.random.default_rng(seed)
     pairs = random_pairs(rng, n, max_terms=3 * n)
@@ -101,7 +101,7 @@ def test_u16_and_f64_paths_agree():
 
 
 @pytest.mark.parametrize("n", [9, 13, 15])
-def test_custom_mixer_random_su2_vs_oracle(n, pass_kernel):
+def test_custom_mixer_random_su2_vs_oracle(n, pass_plan):
     rng = np.random.default_rng(40 + n)
     p = 2
     tables = [[random_su2_coeffs(rng) for _ in range(n)] for _ in range(p)]
