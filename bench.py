@@ -27,6 +27,7 @@ One "step" = one full QAOA objective evaluation: |+>^n -> p x (phase, X mixer)
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -41,6 +42,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BASE_N = 26
+PASS_NAMES = {-1: "phase sweep", 0: "8|0|4", 1: "8|4", 2: "8|0|4|0|8", 3: "8|4|8"}
 METRIC = "QAOA objective evals/sec (LABS/MaxCut n=26–34); achieved HBM GB/s vs peak"
 
 
@@ -272,6 +274,8 @@ def main():
     lay = (_lib.FqLayer * p)(*[_lib.FqLayer(*lt) for lt in layers])
     passes = _lib.load().fq_plan_x_passes(n_local, p, lay)
     n_phase = sum(1 for gi in g if gi != 0.0)
+    P_survey = -(-n_local // 12)
+    survey_bytes = p * (P_survey * 2 * S + Cb) + (S + Cb)
     if world == 1:
         tile_bytes = passes * 2 * S - S + (n_phase + 1) * Cb  # first pass generates |+>, last reads costs for E
         launches = passes + 1
@@ -283,7 +287,41 @@ def main():
         launches = p * (per_layer + (1 if k > 0 else 0)) + 2
         del local_passes
     peak, peak_kind = load_peaks()
-    achieved = tile_bytes / (ms_step / 1e3) / 1e9
+    achieved_step = tile_bytes / (ms_step / 1e3) / 1e9
+
+    # ------------------------------------------------------------ per-launch timing of the pass kernel
+    # CUDA events recorded by libfqaoa between consecutive passes on the launching
+    # stream (option "time_passes"), over `steps` extra steps right after the
+    # timed region; achieved = algorithmic bytes of the passes / their event time.
+    kinds = {}
+    if world == 1:
+        _lib.call("fq_set_option", b"time_passes", 1)
+        info = (ctypes.c_int * (5 * 256))()
+        tms = (ctypes.c_float * 256)()
+        tot_b = tot_ms = 0.0
+        for _ in range(args.steps):
+            step()
+            cnt = _lib.load().fq_last_passes(info, tms, 256)
+            for i in range(cnt):
+                sq, ph, nt, ini, ex = info[5 * i:5 * i + 5]
+                nb = (0 if ini else S) + S + (Cb if (ph or ex) else 0)
+                kd = kinds.setdefault(PASS_NAMES.get(sq, str(sq)) + (" +phase" if ph else "") +
+                                      (" +init" if ini else "") + (" +expect" if ex else ""),
+                                      {"launches": 0, "ms": 0.0, "bytes": 0})
+                kd["launches"] += 1
+                kd["ms"] += tms[i]
+                kd["bytes"] += nb
+                tot_b += nb
+                tot_ms += tms[i]
+        _lib.call("fq_set_option", b"time_passes", 0)
+        for kd in kinds.values():
+            kd["avg_ms"] = kd["ms"] / kd["launches"]
+            kd["GBps"] = kd["bytes"] / (kd["ms"] / 1e3) / 1e9
+            kd["bytes_per_launch"] = kd["bytes"] // kd["launches"]
+            del kd["ms"], kd["bytes"]
+        achieved = tot_b / (tot_ms / 1e3) / 1e9 if tot_ms > 0 else achieved_step
+    else:
+        achieved = achieved_step
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -362,8 +400,14 @@ def main():
                        "parallelism": f"state sharded over {world} GPUs" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": "k_tile_pass (all passes of the step)",
-                         "algorithmic_bytes_per_step": tile_bytes, "passes_per_step": passes if world == 1 else None},
+                         "kernel": "k_pass16 (every tiled pass of the step; per-launch CUDA events)",
+                         "bytes_per_launch": "2*S + C(phase/expectation) - S(|+> generated); S = 16*2^n, "
+                                             "C = cost bytes per amplitude * 2^n",
+                         "achieved_whole_step": achieved_step,
+                         "algorithmic_bytes_per_step": tile_bytes, "passes_per_step": passes if world == 1 else None,
+                         "by_pass_kind": kinds or None,
+                         "survey_model": {"bytes_per_eval": survey_bytes, "evals_per_s_at_peak": peak * 1e9 / survey_bytes,
+                                          "note": "SURVEY.md §8(d): P=ceil(n/12) unfused passes per layer"}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches * args.steps,

@@ -23,3 +23,13 @@ def golden():
     path = os.path.join(ROOT, "tests", "golden", "golden.npz")
     with np.load(path) as z:
         return {k: z[k] for k in z.files}
+
+
+@pytest.fixture(scope="session")
+def golden_large():
+    """Full-size fingerprints of the reference's outputs (scripts/gen_golden_large.py)."""
+    import numpy as np
+
+    path = os.path.join(ROOT, "tests", "golden", "golden_large.npz")
+    with np.load(path) as z:
+        return {k: z[k] for k in z.files}

@@ -1,0 +1,120 @@
+"""Multi-process sharding (ShardedQaoaSimulator, one rank per GPU in
+production) on CPU: world size 2 over gloo, the shard-local work done by a
+test-only backend on the oracle (oracle/, the checker), the orchestration —
+global-qubit split, Alg. 4 exchange order, chunked exchange, exchange counts,
+scalar reductions — is the product code (paper_2309_04841_b200/distributed.py).
+Reference behaviour: distributed.py:103-153, 228-252; tests/test_distributed.py."""
+
+import os
+import socket
+from math import comb, sqrt
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+
+
+class OracleOps:
+    """Shard-local operations for ShardedQaoaSimulator on host tensors (test only)."""
+
+    def fits(self, n_local, bytes_per_amp):
+        return True
+
+    def fits_bytes(self, nbytes):
+        return True
+
+    def precompute(self, poly, base, n_local, compact, keep_f64):
+        pairs = [(t.weight, t.support) for t in poly.terms]
+        return O.precompute_cost_vector(poly.n, pairs, base=base, size=1 << n_local)
+
+    def empty(self, n_local):
+        return torch.empty(1 << n_local, dtype=torch.complex128)
+
+    def uniform(self, n, n_local):
+        return torch.full((1 << n_local,), 1.0 / sqrt(2.0 ** n), dtype=torch.complex128)
+
+    def hamming(self, n, weight, base, n_local):
+        idx = np.arange(base, base + (1 << n_local), dtype=np.int64)
+        pop = np.array([bin(int(i)).count("1") for i in idx])
+        return torch.from_numpy(np.where(pop == weight, 1.0 / sqrt(comb(n, weight)), 0.0).astype(np.complex128))
+
+    def program(self, psi, n_local, kind, layers, costs, init=False, init_amp=0.0):
+        assert kind == "x"
+        st = psi.numpy()
+        if init:
+            st[:] = init_amp
+        for g, b, ph, lo, hi in layers:
+            if ph and g != 0.0:
+                O.apply_phase(st, costs, g)
+            a, bb = O.rx_coeffs(b)
+            for q in range(lo, hi):
+                O.su2_on_pairs(st, a, bb, q)
+
+    def expectation(self, psi, costs):
+        return torch.tensor([O.expectation(psi.numpy(), costs)], dtype=torch.float64)
+
+    def min_cost(self, costs):
+        return torch.tensor([float(costs.min())], dtype=torch.float64)
+
+    def masked_probability(self, psi, costs, cutoff):
+        p = np.abs(psi.numpy()) ** 2
+        return torch.tensor([float(p[costs <= cutoff].sum())], dtype=torch.float64)
+
+
+def _worker(rank, world, port, n, p, chunk, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2309_04841_b200 import instrumentation
+        from paper_2309_04841_b200.distributed import ShardedQaoaSimulator
+        from paper_2309_04841_b200.problems import labs_terms
+
+        rng = np.random.default_rng(5)
+        g, b = rng.uniform(0, 1, p), rng.uniform(0, 1, p)
+        sim = ShardedQaoaSimulator(labs_terms(n), local_ops=OracleOps(), chunk_bytes=chunk)
+        instrumentation.reset()
+        E = sim.simulate_qaoa(g, b)
+        ov = sim.overlap()
+        shards = [torch.empty_like(sim.shard) for _ in range(world)]
+        dist.all_gather(shards, sim.shard)
+        q.put((rank, E, ov, sim.exchange_count, instrumentation.get("exchange"),
+               torch.cat(shards).numpy() if rank == 0 else None))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("n,p,chunk", [(10, 3, None), (11, 2, 4096)])
+def test_sharded_world2_matches_single_node(n, p, chunk):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, p, chunk, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    out.sort(key=lambda t: t[0])
+    rng = np.random.default_rng(5)
+    g, b = rng.uniform(0, 1, p), rng.uniform(0, 1, p)
+    costs = O.precompute_cost_vector(n, O.labs_terms(n))
+    ref = O.simulate(costs, g, b)
+    e_ref, ov_ref = O.expectation(ref, costs), O.overlap(ref, costs)
+    for rank, E, ov, ex, ex_counter, state in out:
+        assert E == pytest.approx(e_ref, rel=1e-12, abs=1e-12)  # all-reduced on every rank
+        assert ov == pytest.approx(ov_ref, abs=1e-12)
+        assert ex == 2 * p and ex_counter == 2 * p  # Alg. 4: two exchanges per X layer
+    np.testing.assert_allclose(out[0][5], ref, rtol=0, atol=1e-12)
