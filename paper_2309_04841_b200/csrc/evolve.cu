@@ -35,6 +35,8 @@
 //    in its shared-memory / FP64 rounds.
 //  * States of n <= 12 qubits run the entire program in one CTA (smem-resident),
 //    which is also the batched multi-parameter path for optimiser loops.
+#include <cudaTypedefs.h>
+
 #include "pass.cuh"
 
 namespace fq {
@@ -350,6 +352,76 @@ static std::vector<PlannedPass> plan_x(int n, int nl, const fq_layer *layers, st
     return best;
 }
 
+// ---- tensor maps for the tile prefetch (driver entry point fetched through the runtime; no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// Describe one tile (12 physical index bits) of a 2^n vector as a TMA box:
+// runs of tile bits become box dims (full extent, <= 256 elements each), runs
+// of outer bits become box-1 dims whose coordinate comes from the tile number.
+// `per_amp` elements of `elem_bytes` per amplitude (state: 2 doubles).
+// Returns the rank (0 if the layout cannot be expressed: rank > 5, rows or
+// strides not multiples of 16 B, or no driver entry point).
+static int build_tile_map(CUtensorMap *map, const void *gaddr, int n, const int *tile_pos, CUtensorMapDataType dt,
+                          int elem_bytes, int per_amp, int *outer_shift, int *outer_bits) {
+    auto fn = encode_fn();
+    if (!fn || !gaddr) return 0;
+    bool is_tile[64] = {};
+    for (int i = 0; i < kTileBits; ++i) is_tile[tile_pos[i]] = true;
+    if (!is_tile[0]) return 0;
+    struct Dim { bool tile; int start, len; };
+    std::vector<Dim> dims;
+    const int cap0 = (per_amp == 2) ? 7 : 8;
+    for (int b = 0; b < n;) {
+        int e = b;
+        while (e < n && is_tile[e] == is_tile[b]) ++e;
+        if (is_tile[b]) {
+            for (int at = b; at < e;) {
+                const int len = std::min(dims.empty() ? cap0 : 8, e - at);
+                dims.push_back({true, at, len});
+                at += len;
+            }
+        } else {
+            dims.push_back({false, b, e - b});
+        }
+        b = e;
+    }
+    if (dims.size() > 5) return 0;
+    const int rank = (int)dims.size();
+    cuuint64_t gdim[5], gstride[5];
+    cuuint32_t box[5], estr[5];
+    int shift = 0;
+    for (int d = 0; d < rank; ++d) {
+        gdim[d] = (cuuint64_t)(d == 0 ? per_amp : 1) << dims[d].len;
+        box[d] = dims[d].tile ? (cuuint32_t)gdim[d] : 1u;
+        estr[d] = 1;
+        if (d > 0) {
+            gstride[d - 1] = ((cuuint64_t)1 << dims[d].start) * per_amp * elem_bytes;
+            if (gstride[d - 1] % 16) return 0;
+        }
+        outer_shift[d] = dims[d].tile ? 0 : shift;
+        outer_bits[d] = dims[d].tile ? 0 : dims[d].len;
+        if (!dims[d].tile) shift += dims[d].len;
+    }
+    if ((box[0] * (cuuint32_t)elem_bytes) % 16) return 0;
+    for (int d = rank; d < 5; ++d) outer_shift[d] = outer_bits[d] = 0;
+    CUresult r = fn(map, dt, (cuuint32_t)rank, const_cast<void *>(gaddr), gdim, gstride, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? rank : 0;
+}
+
 // Mask class of a pass (template K of k_pass16) from its per-round masks.
 static int mask_class(int seq, const unsigned char *maskA) {
     const int nr = seq_rounds(seq);
@@ -369,16 +441,16 @@ static int mask_class(int seq, const unsigned char *maskA) {
 
 // RX forms are compile-time for set A and for set B of heavy passes (set B of
 // a light pass runs in the run-time form: it only occurs for gamma = 0 layers).
-static int launch_pass(int mix, int cost, const PassParams &P, int seq, int ph, int ma, int mb, int grid,
-                       cudaStream_t st) {
+static int launch_pass(int mix, int cost, const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb,
+                       int grid, cudaStream_t st) {
     const int k = mask_class(seq, P.maskA);
-    if (mix == MIX_SU2) return launch_pass_su2(P, cost, seq, ph, mb == 2 ? 2 : 3, k, grid, st);
+    if (mix == MIX_SU2) return launch_pass_su2(P, M, cost, seq, ph, mb == 2 ? 2 : 3, k, grid, st);
     if (!seq_heavy(seq) && mb != 2) mb = 3;
     if (cost == FQ_COST_U16)
-        return seq_heavy(seq) ? launch_pass_rx_u16_heavy(P, seq, ph, ma, mb, k, grid, st)
-                              : launch_pass_rx_u16_light(P, seq, ph, ma, mb, k, grid, st);
-    return seq_heavy(seq) ? launch_pass_rx_f64_heavy(P, seq, ph, ma, mb, k, grid, st)
-                          : launch_pass_rx_f64_light(P, seq, ph, ma, mb, k, grid, st);
+        return seq_heavy(seq) ? launch_pass_rx_u16_heavy(P, M, seq, ph, ma, mb, k, grid, st)
+                              : launch_pass_rx_u16_light(P, M, seq, ph, ma, mb, k, grid, st);
+    return seq_heavy(seq) ? launch_pass_rx_f64_heavy(P, M, seq, ph, ma, mb, k, grid, st)
+                          : launch_pass_rx_f64_light(P, M, seq, ph, ma, mb, k, grid, st);
 }
 
 static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
@@ -504,8 +576,21 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
         P.run_bits = 0;
         while (P.run_bits < kTileBits && g.tile_pos[P.run_bits] == P.run_bits) ++P.run_bits;
         P.pf_cost = (ph != 0 || P.expect) ? 1 : 0;
+        PassMaps M;
+        std::memset(&M, 0, sizeof M);
+        if (P.pf_dist > 0) {
+            P.sm_rank = build_tile_map(&M.state, psi, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2, P.sm_shift,
+                                       P.sm_bits);
+            if (P.pf_cost)
+                P.cm_rank = d->cost_kind == FQ_COST_F64
+                                ? build_tile_map(&M.cost, d->costs, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 1,
+                                                 P.cm_shift, P.cm_bits)
+                                : build_tile_map(&M.cost, d->costs, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, 1,
+                                                 P.cm_shift, P.cm_bits);
+            if (P.sm_rank == 0 && P.cm_rank == 0) P.pf_dist = 0;
+        }
         const int ma = P.A.mode, mb = two ? P.B.mode : 2;
-        const int s = launch_pass(mix, d->cost_kind, P, sq, ph, ma, mb, grid, st);
+        const int s = launch_pass(mix, d->cost_kind, P, M, sq, ph, ma, mb, grid, st);
         if (s) return s;
         g_last_plan.push_back({sq, ph, (int)g.targets.size(), P.init, P.expect});
         if (P.expect) {

@@ -8,6 +8,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace fq {
@@ -63,6 +65,8 @@ struct PassParams {
     int pf_dist;              // L2 prefetch distance in grid strides (0: off)
     int run_bits;             // tile bits 0..run_bits-1 sit at physical bits 0..run_bits-1 (contiguous runs)
     int pf_cost;              // also prefetch the cost slice of the tile
+    int sm_rank, sm_shift[5], sm_bits[5];  // state tensor map: rank, outer-dim coordinate = (t >> shift) & (2^bits - 1)
+    int cm_rank, cm_shift[5], cm_bits[5];  // cost tensor map (cm_rank = 0: no cost prefetch)
     int probe;                // development: 1 no cost loads, 2 fixed table row, 4 no phase multiply
     long long roff[3][kRegs]; // per pattern: physical offset of register i (read from the constant bank,
                               // so no register holds the 16 offsets across the rounds)
@@ -245,28 +249,52 @@ __device__ __forceinline__ long long tile_base(const PassParams &P, long long t)
     return base;
 }
 
-// L2 prefetch of a future tile: the tile is 2^(12-s) contiguous runs of 2^s
-// amplitudes (s = P.run_bits); one cp.async.bulk.prefetch per run, spread
-// over the CTA's threads, so the tile's loads later hit L2.
-__device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+// L2 prefetch of a future tile with ONE instruction: the tile is described
+// by a tensor map (runs of tile bits = full box dims, runs of outer bits =
+// box-1 dims whose coordinates come from the tile number), and
+// cp.async.bulk.prefetch.tensor (SASS UTMAPF) fetches the whole strided box
+// into L2 while the CTA is busy with the current tile.
+__device__ __forceinline__ void tile_coords(long long t, int rank, const int *shift, const int *bits, int *c) {
+#pragma unroll
+    for (int d = 0; d < 5; ++d)
+        c[d] = (d < rank && bits[d] > 0) ? (int)((t >> shift[d]) & ((1LL << bits[d]) - 1)) : 0;
 }
 
-template <int COST>
-__device__ __forceinline__ void prefetch_tile(const PassParams &P, long long t, bool state) {
-    const int s = P.run_bits;
-    const int runs = 1 << (kTileBits - s);
-    const long long base = tile_base(P, t);
-    constexpr int cb = COST == FQ_COST_F64 ? 8 : 2;
-    const int cbytes = cb << s;
-    for (int r = threadIdx.x; r < runs; r += blockDim.x) {
-        long long off = base;
-#pragma unroll 1
-        for (int j = 0; j < kTileBits - s; ++j)
-            if ((r >> j) & 1) off += 1LL << P.tile_pos[s + j];
-        if (state) bulk_prefetch_l2(P.psi + off, 16u << s);
-        if (P.pf_cost && (cbytes & 15) == 0)
-            bulk_prefetch_l2(static_cast<const char *>(P.costs) + off * cb, (uint32_t)cbytes);
+__device__ __forceinline__ void tensor_prefetch_l2(const CUtensorMap *map, int rank, const int *c) {
+    const uint64_t m = reinterpret_cast<uint64_t>(map);
+    switch (rank) {
+        case 1:
+            asm volatile("cp.async.bulk.prefetch.tensor.1d.L2.global.tile [%0, {%1}];" ::"l"(m), "r"(c[0]) : "memory");
+            break;
+        case 2:
+            asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(m), "r"(c[0]), "r"(c[1])
+                         : "memory");
+            break;
+        case 3:
+            asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(m), "r"(c[0]),
+                         "r"(c[1]), "r"(c[2]) : "memory");
+            break;
+        case 4:
+            asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(m), "r"(c[0]),
+                         "r"(c[1]), "r"(c[2]), "r"(c[3]) : "memory");
+            break;
+        default:
+            asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(m),
+                         "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]) : "memory");
+            break;
+    }
+}
+
+__device__ __forceinline__ void prefetch_tile(const PassParams &P, const CUtensorMap *ms, const CUtensorMap *mc,
+                                              long long t, bool state) {
+    int c[5];
+    if (state && P.sm_rank > 0) {
+        tile_coords(t, P.sm_rank, P.sm_shift, P.sm_bits, c);
+        tensor_prefetch_l2(ms, P.sm_rank, c);
+    }
+    if (P.pf_cost && P.cm_rank > 0) {
+        tile_coords(t, P.cm_rank, P.cm_shift, P.cm_bits, c);
+        tensor_prefetch_l2(mc, P.cm_rank, c);
     }
 }
 
@@ -296,7 +324,9 @@ __device__ __forceinline__ int round_mask(const unsigned char *rt, int r) {
 //       the butterfly code branch-free (run-time masks force register moves at
 //       every merge point).
 template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K>
-__global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ PassParams P) {
+__global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ PassParams P,
+                                                        const __grid_constant__ CUtensorMap tm_state,
+                                                        const __grid_constant__ CUtensorMap tm_cost) {
     extern __shared__ double2 smem[];
     double2 *tile = smem;
     double2 *tlo = smem + kTilePadded;
@@ -319,17 +349,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
     const long long thrL = LAST == PAT8 ? thr8 : thr4;
     double eacc = 0.0;
 
-    if (P.pf_dist > 1) {  // prologue: tiles 1 .. pf_dist-1 of this CTA
+    const bool pf = P.pf_dist > 0 && tid == 0;
+    if (pf) {  // prologue: tiles 1 .. pf_dist-1 of this CTA
         for (int d = 1; d < P.pf_dist; ++d) {
             const long long tp = blockIdx.x + (long long)d * gridDim.x;
-            if (tp < P.n_tiles) prefetch_tile<COST>(P, tp, !P.init);
+            if (tp < P.n_tiles) prefetch_tile(P, &tm_state, &tm_cost, tp, !P.init);
         }
     }
     for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
         const long long base = tile_base(P, t);
-        if (P.pf_dist > 0) {
+        if (pf) {
             const long long tp = t + (long long)P.pf_dist * gridDim.x;
-            if (tp < P.n_tiles) prefetch_tile<COST>(P, tp, !P.init);
+            if (tp < P.n_tiles) prefetch_tile(P, &tm_state, &tm_cost, tp, !P.init);
         }
         double2 v[kRegs];
         CostRaw<COST> raw[kRegs];  // cost entries of the phase round, loaded with the state
@@ -427,8 +458,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------- launch
+struct PassMaps {
+    alignas(64) CUtensorMap state;
+    alignas(64) CUtensorMap cost;
+};
+
 template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K>
-static int launch_pass16(const PassParams &P, int grid, cudaStream_t st) {
+static int launch_pass16(const PassParams &P, const PassMaps &M, int grid, cudaStream_t st) {
     static bool configured = false;
     const size_t smem = (size_t)(kTilePadded + (kTableLo + kMaxTableHi) * kCopies) * sizeof(double2);
     if (!configured) {
@@ -437,7 +473,7 @@ static int launch_pass16(const PassParams &P, int grid, cudaStream_t st) {
         configured = true;
     }
     const size_t need = (size_t)(kTilePadded + (kTableLo + P.table_hi) * kCopies) * sizeof(double2);
-    k_pass16<MIX, COST, SEQ, PH, MA, MB, K><<<grid, kThreads, need, st>>>(P);
+    k_pass16<MIX, COST, SEQ, PH, MA, MB, K><<<grid, kThreads, need, st>>>(P, M.state, M.cost);
     FQ_LAUNCHED("k_pass16");
     return FQ_OK;
 }
@@ -447,17 +483,17 @@ static int launch_pass16(const PassParams &P, int grid, cudaStream_t st) {
 // caller); a mask class k without an instantiation runs with the run-time
 // masks (K_RUNTIME), which PassParams always carries.
 template <int MIX, int COST, int SEQ>
-static int select_seq(const PassParams &P, int ph, int ma, int mb, int k, int grid, cudaStream_t st) {
+static int select_seq(const PassParams &P, const PassMaps &M, int ph, int ma, int mb, int k, int grid, cudaStream_t st) {
     constexpr bool kHigh = SEQ == SEQ_84 || SEQ == SEQ_848;
 #define FQ_K(PHV, MAV, MBV)                                                                                  \
     if (ph == PHV && ma == MAV && mb == MBV) {                                                               \
-        if (k == K_FULL) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_FULL>(P, grid, st);          \
+        if (k == K_FULL) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_FULL>(P, M, grid, st);          \
         if constexpr (kHigh && MIX == MIX_RX) {                                                              \
-            if (k == 1) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 1>(P, grid, st);                \
-            if (k == 2) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 2>(P, grid, st);                \
-            if (k == 3) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 3>(P, grid, st);                \
+            if (k == 1) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 1>(P, M, grid, st);                \
+            if (k == 2) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 2>(P, M, grid, st);                \
+            if (k == 3) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 3>(P, M, grid, st);                \
         }                                                                                                    \
-        return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_RUNTIME>(P, grid, st);                        \
+        return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_RUNTIME>(P, M, grid, st);                        \
     }
     if constexpr (seq_heavy(SEQ)) {
         if constexpr (MIX == MIX_RX) {
@@ -475,10 +511,10 @@ static int select_seq(const PassParams &P, int ph, int ma, int mb, int k, int gr
 }
 
 // Instantiation units (pass_*.cu), compiled in parallel.
-int launch_pass_rx_u16_light(const PassParams &P, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
-int launch_pass_rx_u16_heavy(const PassParams &P, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
-int launch_pass_rx_f64_light(const PassParams &P, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
-int launch_pass_rx_f64_heavy(const PassParams &P, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
-int launch_pass_su2(const PassParams &P, int cost, int seq, int ph, int mb, int k, int grid, cudaStream_t st);
+int launch_pass_rx_u16_light(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
+int launch_pass_rx_u16_heavy(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
+int launch_pass_rx_f64_light(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
+int launch_pass_rx_f64_heavy(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
+int launch_pass_su2(const PassParams &P, const PassMaps &M, int cost, int seq, int ph, int mb, int k, int grid, cudaStream_t st);
 
 }  // namespace fq

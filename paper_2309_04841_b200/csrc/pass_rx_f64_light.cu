@@ -3,9 +3,9 @@
 
 namespace fq {
 
-int launch_pass_rx_f64_light(const PassParams &P, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st) {
-    if (seq == SEQ_840) return select_seq<MIX_RX, FQ_COST_F64, SEQ_840>(P, ph, ma, mb, k, grid, st);
-    if (seq == SEQ_84) return select_seq<MIX_RX, FQ_COST_F64, SEQ_84>(P, ph, ma, mb, k, grid, st);
+int launch_pass_rx_f64_light(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st) {
+    if (seq == SEQ_840) return select_seq<MIX_RX, FQ_COST_F64, SEQ_840>(P, M, ph, ma, mb, k, grid, st);
+    if (seq == SEQ_84) return select_seq<MIX_RX, FQ_COST_F64, SEQ_84>(P, M, ph, ma, mb, k, grid, st);
     set_error("launch_pass_rx_f64_light: bad round program %d", seq);
     return FQ_ERR_UNSUPPORTED;
 }

@@ -3,9 +3,9 @@
 
 namespace fq {
 
-int launch_pass_su2(const PassParams &P, int cost, int seq, int ph, int mb, int k, int grid, cudaStream_t st) {
+int launch_pass_su2(const PassParams &P, const PassMaps &M, int cost, int seq, int ph, int mb, int k, int grid, cudaStream_t st) {
 #define FQ_S(C, Q) \
-    if (cost == C && seq == Q) return select_seq<MIX_SU2, C, Q>(P, ph, 0, mb, k, grid, st);
+    if (cost == C && seq == Q) return select_seq<MIX_SU2, C, Q>(P, M, ph, 0, mb, k, grid, st);
     FQ_S(FQ_COST_U16, SEQ_840) FQ_S(FQ_COST_U16, SEQ_84) FQ_S(FQ_COST_U16, SEQ_84048) FQ_S(FQ_COST_U16, SEQ_848)
     FQ_S(FQ_COST_F64, SEQ_840) FQ_S(FQ_COST_F64, SEQ_84) FQ_S(FQ_COST_F64, SEQ_84048) FQ_S(FQ_COST_F64, SEQ_848)
 #undef FQ_S
