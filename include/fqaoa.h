@@ -186,6 +186,10 @@ int fq_qaoa_evolve_batched(int n, int mixer, const void *costs, int cost_kind, d
  * byte model in bench.py / DESIGN.md). */
 int fq_plan_x_passes(int n, int n_layers, const fq_layer *layers);
 
+/* HBM passes per layer of the tiled XY program (ring / complete gate order of
+ * reference mixers.py:109-125) at n qubits; 1 for n <= 12 (on chip), -1 for other kinds. */
+int fq_plan_xy_passes(int n, int mixer);
+
 /* Passes of the last tiled X/custom program run on this host thread's
  * process: returns the pass count; for i < max fills info[5*i..5*i+4] =
  * (round program: 0 = 8|0|4, 1 = 8|4, 2 = 8|0|4|0|8, 3 = 8|4|8, -1 = standalone
@@ -200,7 +204,8 @@ int fq_last_passes(int *info, float *ms, int max);
  *   "fuse"         fuse the passes at layer boundaries (default 1)
  *   "phase_tables" uint16 phase through shared-memory tables (default 1, 0 = sincos)
  *   "plan"         group plan: -1 cost model (default), 0 legacy, 1 small fusion groups
- *   "time_passes"  record a CUDA event after every pass (read with fq_last_passes) */
+ *   "time_passes"  record a CUDA event after every pass (read with fq_last_passes)
+ *   "xy_tiled"     tiled XY passes (default 1; 0 = one pair kernel per gate) */
 int fq_set_option(const char *name, int value);
 
 #ifdef __cplusplus

@@ -58,6 +58,7 @@ _SIGS = {
     "fq_plan_x_passes": ([I, I, ctypes.POINTER(FqLayer)], I),
     "fq_set_option": ([ctypes.c_char_p, I], I),
     "fq_last_passes": ([P, P, I], I),
+    "fq_plan_xy_passes": ([I, I], I),
 }
 
 EXPORTED = tuple(_SIGS)

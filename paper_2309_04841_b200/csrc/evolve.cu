@@ -617,10 +617,20 @@ static void xy_gates(int n, int kind, std::vector<std::pair<int, int>> &g) {
     }
 }
 
+int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>> &gates, cudaStream_t st,
+                 int *passes_out);
+int plan_xy_passes(int n, const std::vector<std::pair<int, int>> &gates);
+static int g_xy_tiled = 1;   // tiled XY passes (0: one pair kernel per gate, the reference's structure)
+
 static int run_xy_program(const fq_evolve_desc *d, cudaStream_t st) {
     const int n = d->n;
     const long long size = 1LL << n;
     double2 *psi = static_cast<double2 *>(d->psi);
+    if (g_xy_tiled) {
+        std::vector<std::pair<int, int>> gates;
+        xy_gates(n, d->mixer, gates);
+        return run_xy_tiled(d, gates, st, nullptr);
+    }
     if (d->init) {
         int s = fq_init_state(psi, size, -1, d->init_amp, 0, st);
         if (s) return s;
@@ -764,6 +774,7 @@ int fq_set_option(const char *name, int value) {
         {"phase_tables", &g_phase_tables, 0, 1},  // uint16 phase via smem tables (else sincos)
         {"plan", &g_plan, -1, 1},           // group plan: -1 cost model, 0 legacy, 1 small fusion groups
         {"time_passes", &g_time_passes, 0, 1},  // CUDA events around every pass (fq_last_passes)
+        {"xy_tiled", &g_xy_tiled, 0, 1},    // tiled XY passes (0: one kernel per gate)
         {"probe", &g_probe, 0, 7},          // development: isolate phase costs (results invalid when != 0)
     };
     for (auto &o : opts) {
@@ -784,6 +795,14 @@ int fq_plan_x_passes(int n, int n_layers, const fq_layer *layers) {
     if (n <= kTileBits) return n_layers > 0 ? 1 : 0;
     std::vector<Group> groups;
     return (int)plan_x(n, n_layers, layers, groups, g_fuse != 0).size();
+}
+
+int fq_plan_xy_passes(int n, int mixer) {
+    if (n <= kTileBits) return 1;
+    if (mixer != FQ_MIXER_XY_RING && mixer != FQ_MIXER_XY_COMPLETE) return -1;
+    std::vector<std::pair<int, int>> gates;
+    xy_gates(n, mixer, gates);
+    return plan_xy_passes(n, gates);
 }
 
 int fq_last_passes(int *info, float *ms, int max) {

@@ -1,0 +1,467 @@
+// Tiled XY mixers (reference mixers.py:94-137, _kernels.py:30-48): the
+// documented gate sequence of a layer (ring: even pairs, odd pairs, wrap;
+// complete: lexicographic, mixers.py:5-15) is cut into HBM passes.  A pass
+// owns a set of <= 12 tile bits (the gates' qubits plus low spectator bits
+// for coalescing) and applies, tile by tile, every gate of a dependency-closed
+// subsequence whose qubits are tile bits — order preserved wherever two
+// gates share a qubit (gates on disjoint pairs commute).  Inside a pass the
+// gates run in register "rounds": 16 amplitudes per thread = 4 tile bits in
+// registers, each gate's two bits in the same round, XOR-swizzled
+// shared-memory transposes between rounds.  The layer's phase rides in the
+// first pass, the expectation in the program's last pass.
+//
+// Reference cost: one full state sweep per gate (26 per ring layer, 325 per
+// complete layer at n = 26); here a handful of passes per layer.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "pass.cuh"
+
+namespace fq {
+
+constexpr int kXyMaxRounds = 24;
+constexpr int kXyMaxGates = 6;  // C(4, 2): distinct pairs of one 4-bit register set
+
+struct XyRound {
+    unsigned char reg[4];         // tile bits held in registers (register index bit j <- tile bit reg[j])
+    unsigned char tb[8];          // thread bit k <- tile bit tb[k]
+    unsigned char ngates;
+    unsigned char gate[kXyMaxGates];  // code = 4 * a + b: lo qubit at register bit a, hi qubit at b
+    unsigned short sreg[kRegs];   // swizzled smem slot of register i's tile-index part
+};
+
+struct XyParams {
+    double2 *psi;
+    const void *costs;
+    double cost_scale, cost_offset;
+    double *partials;
+    double init_amp;
+    double gamma;
+    double c, s;  // cos(beta), sin(beta)
+    long long n_tiles;
+    int tile_pos[kTileBits];
+    long long roff_first[kRegs], roff_last[kRegs];  // physical offsets of the registers, first / last round
+    int init, expect, table_hi;
+    int nrounds;
+    XyRound rounds[kXyMaxRounds];
+};
+
+// XOR swizzle of a 12-bit tile index (bijective; GF(2)-linear, so the slot of
+// thread part | register part is the XOR of the parts' slots).  The bank group
+// of slot e is fold3(e): a quarter-warp whose three lane bits sit on tile bits
+// of distinct residues mod 3 is conflict-free.
+__host__ __device__ __forceinline__ int xy_slot(int e) { return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7); }
+
+// x_lo' = c x_lo - i s x_hi ; x_hi' = -i s x_lo + c x_hi   (reference _kernels.py:44-47)
+template <int A, int B>
+__device__ __forceinline__ void xy_gate(double2 (&v)[kRegs], double c, double s) {
+#pragma unroll
+    for (int i = 0; i < kRegs; ++i) {
+        if (((i >> A) & 1) && !((i >> B) & 1)) {
+            const int j = i ^ (1 << A) ^ (1 << B);
+            const double2 xl = v[i], xh = v[j];
+            v[i] = make_double2(fma(c, xl.x, s * xh.y), fma(c, xl.y, -s * xh.x));
+            v[j] = make_double2(fma(s, xl.y, c * xh.x), fma(c, xh.y, -s * xl.x));
+        }
+    }
+}
+
+__device__ __forceinline__ void xy_apply(double2 (&v)[kRegs], int code, double c, double s) {
+    switch (code) {
+        case 1: xy_gate<0, 1>(v, c, s); break;
+        case 2: xy_gate<0, 2>(v, c, s); break;
+        case 3: xy_gate<0, 3>(v, c, s); break;
+        case 4: xy_gate<1, 0>(v, c, s); break;
+        case 6: xy_gate<1, 2>(v, c, s); break;
+        case 7: xy_gate<1, 3>(v, c, s); break;
+        case 8: xy_gate<2, 0>(v, c, s); break;
+        case 9: xy_gate<2, 1>(v, c, s); break;
+        case 11: xy_gate<2, 3>(v, c, s); break;
+        case 12: xy_gate<3, 0>(v, c, s); break;
+        case 13: xy_gate<3, 1>(v, c, s); break;
+        case 14: xy_gate<3, 2>(v, c, s); break;
+        default: break;
+    }
+}
+
+// tile-index part of this thread in round r (thread bit k -> tile bit tb[k])
+__device__ __forceinline__ int xy_tpart(const XyRound &R, int tid) {
+    int e = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) e |= ((tid >> k) & 1) << R.tb[k];
+    return e;
+}
+
+__device__ __forceinline__ long long xy_tphys(const XyParams &P, const XyRound &R, int tid) {
+    long long o = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if ((tid >> k) & 1) o += 1LL << P.tile_pos[R.tb[k]];
+    return o;
+}
+
+__device__ __forceinline__ long long xy_tile_base(const int *tile_pos, long long t) {
+    long long base = t;
+#pragma unroll
+    for (int j = 0; j < kTileBits; ++j) {
+        const int p = tile_pos[j];
+        base = ((base >> p) << (p + 1)) | (base & ((1LL << p) - 1));
+    }
+    return base;
+}
+
+template <int COST>
+__device__ __forceinline__ double2 xy_phase(const XyParams &P, CostRaw<COST> raw, const double2 *tlo,
+                                            const double2 *thi) {
+    if constexpr (COST == FQ_COST_F64) {
+        return phase_f64(raw, P.gamma);
+    } else {
+        if (P.table_hi == 0) return phase_sincos_u16(raw, P.cost_scale, P.cost_offset, P.gamma);
+        const int cp = threadIdx.x & (kCopies - 1);
+        return cmul(thi[(raw >> 6) * kCopies + cp], tlo[(raw & 63) * kCopies + cp]);
+    }
+}
+
+template <int COST, int PH>
+__global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__ XyParams P) {
+    extern __shared__ double2 smem[];
+    double2 *tile = smem;
+    double2 *tlo = smem + kTile;
+    double2 *thi = tlo + kTableLo * kCopies;
+    __shared__ double red[kThreads / 32];
+    const int tid = threadIdx.x;
+    if (COST == FQ_COST_U16 && PH) {
+        if (P.table_hi > 0) build_phase_tables(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
+        __syncthreads();
+    }
+    const long long thr_first = xy_tphys(P, P.rounds[0], tid);
+    const long long thr_last = xy_tphys(P, P.rounds[P.nrounds - 1], tid);
+    double eacc = 0.0;
+    for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+        const long long base = xy_tile_base(P.tile_pos, t);
+        double2 v[kRegs];
+        if (P.init) {
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i) v[i] = make_double2(P.init_amp, 0.0);
+        } else {
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i) v[i] = ld_stream(P.psi + base + thr_first + P.roff_first[i]);
+        }
+        if (PH) {
+            CostRaw<COST> raw[kRegs];
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i) {
+                const long long k = base + thr_first + P.roff_first[i];
+                if constexpr (COST == FQ_COST_F64) raw[i] = static_cast<const double *>(P.costs)[k];
+                else raw[i] = static_cast<const unsigned short *>(P.costs)[k];
+            }
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i)
+                v[i] = cmul(v[i], xy_phase<COST>(P, raw[i], tlo, thi));
+        }
+        for (int r = 0; r < P.nrounds; ++r) {
+            const XyRound &R = P.rounds[r];
+            if (r > 0) {  // transpose from round r-1's pattern to round r's
+                const XyRound &Q = P.rounds[r - 1];
+                const int sq = xy_slot(xy_tpart(Q, tid));
+                __syncthreads();
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) tile[sq ^ Q.sreg[i]] = v[i];
+                __syncthreads();
+                const int sr = xy_slot(xy_tpart(R, tid));
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) v[i] = tile[sr ^ R.sreg[i]];
+            }
+            for (int g = 0; g < R.ngates; ++g) xy_apply(v, R.gate[g], P.c, P.s);
+        }
+#pragma unroll
+        for (int i = 0; i < kRegs; ++i) {
+            const long long k = base + thr_last + P.roff_last[i];
+            if (P.expect) {
+                double cv;
+                if constexpr (COST == FQ_COST_F64) cv = static_cast<const double *>(P.costs)[k];
+                else cv = decode_u16(static_cast<const unsigned short *>(P.costs)[k], P.cost_scale, P.cost_offset);
+                eacc += cv * (v[i].x * v[i].x + v[i].y * v[i].y);
+            }
+            st_stream(P.psi + k, v[i]);
+        }
+    }
+    if (P.expect) {
+        const double sum = block_sum<kThreads>(eacc, red);
+        if (tid == 0) P.partials[blockIdx.x] = sum;
+    }
+}
+
+// ---------------------------------------------------------------- host scheduler
+struct XyPassPlan {
+    std::vector<int> tile;                          // 12 physical bits, ascending
+    std::vector<std::vector<int>> round_bits;       // tile-bit indices in registers, per round
+    std::vector<std::vector<std::pair<int, int>>> round_gates;  // (lo qubit, hi qubit), per round
+};
+
+static int run_bits_of(const std::vector<int> &tile) {
+    int r = 0;
+    while (r < (int)tile.size() && tile[r] == r) ++r;
+    return r;
+}
+
+static std::vector<int> tile_for(int n, const std::vector<int> &targets) {
+    std::vector<int> bits = targets;
+    for (int q = 0; q < n && (int)bits.size() < kTileBits; ++q)
+        if (std::find(targets.begin(), targets.end(), q) == targets.end()) bits.push_back(q);
+    std::sort(bits.begin(), bits.end());
+    return bits;
+}
+
+// Greedy dependency-respecting cut of an ordered gate list: scan the remaining
+// gates in order; a gate joins the current group if none of its qubits was
+// touched by a gate left behind (it would have to wait for it) and its qubits
+// fit the capacity test; a gate left behind blocks its qubits.
+template <typename Fits>
+static std::vector<std::vector<int>> cut_groups(const std::vector<std::pair<int, int>> &gates, std::vector<int> idx,
+                                                Fits fits) {
+    std::vector<std::vector<int>> groups;
+    while (!idx.empty()) {
+        std::vector<int> taken, rest, qubits;
+        std::vector<char> blocked(64, 0);
+        for (int gi : idx) {
+            const int a = gates[gi].first, b = gates[gi].second;
+            bool ok = !blocked[a] && !blocked[b];
+            if (ok) {
+                std::vector<int> q2 = qubits;
+                if (std::find(q2.begin(), q2.end(), a) == q2.end()) q2.push_back(a);
+                if (std::find(q2.begin(), q2.end(), b) == q2.end()) q2.push_back(b);
+                ok = fits(q2);
+                if (ok) qubits = q2;
+            }
+            if (ok) {
+                taken.push_back(gi);
+            } else {
+                rest.push_back(gi);
+                blocked[a] = blocked[b] = 1;
+            }
+        }
+        groups.push_back(taken);
+        idx = rest;
+    }
+    return groups;
+}
+
+static std::vector<XyPassPlan> plan_xy(int n, const std::vector<std::pair<int, int>> &gates) {
+    std::vector<int> all(gates.size());
+    for (size_t i = 0; i < gates.size(); ++i) all[i] = (int)i;
+    // passes: the tile (targets + spectators) must keep runs of >= 16 amplitudes
+    auto pass_fits = [&](const std::vector<int> &q) {
+        return (int)q.size() <= kTileBits && run_bits_of(tile_for(n, q)) >= 4;
+    };
+    std::vector<XyPassPlan> plans;
+    for (auto &pg : cut_groups(gates, all, pass_fits)) {
+        XyPassPlan pl;
+        std::vector<int> q;
+        for (int gi : pg) {
+            for (int x : {gates[gi].first, gates[gi].second})
+                if (std::find(q.begin(), q.end(), x) == q.end()) q.push_back(x);
+        }
+        pl.tile = tile_for(n, q);
+        auto tbit = [&](int qubit) { return (int)(std::find(pl.tile.begin(), pl.tile.end(), qubit) - pl.tile.begin()); };
+        // rounds: 4 register bits
+        for (auto &rg : cut_groups(gates, pg, [](const std::vector<int> &qq) { return qq.size() <= 4; })) {
+            std::vector<int> bits;
+            std::vector<std::pair<int, int>> gl;
+            for (int gi : rg) {
+                for (int x : {gates[gi].first, gates[gi].second})
+                    if (std::find(bits.begin(), bits.end(), tbit(x)) == bits.end()) bits.push_back(tbit(x));
+                gl.push_back(gates[gi]);
+            }
+            // pad with spectator-most (highest unused) tile bits so loads/stores keep lanes on the low bits
+            for (int b = kTileBits - 1; (int)bits.size() < 4 && b >= 0; --b)
+                if (std::find(bits.begin(), bits.end(), b) == bits.end()) bits.push_back(b);
+            pl.round_bits.push_back(bits);
+            pl.round_gates.push_back(gl);
+        }
+        // load / store rounds keep the warp's lanes on tile bits 0..4 (coalesced): if the
+        // first (last) round holds one of them in registers, add a gate-free round before (after)
+        auto low_ok = [](const std::vector<int> &bits) {
+            for (int b : bits)
+                if (b < 5) return false;
+            return true;
+        };
+        const std::vector<int> top = {8, 9, 10, 11};
+        if (!low_ok(pl.round_bits.front())) {
+            pl.round_bits.insert(pl.round_bits.begin(), top);
+            pl.round_gates.insert(pl.round_gates.begin(), std::vector<std::pair<int, int>>());
+        }
+        if (!low_ok(pl.round_bits.back())) {
+            pl.round_bits.push_back(top);
+            pl.round_gates.push_back({});
+        }
+        // more rounds than one launch carries: consecutive chunks over the same tile
+        constexpr int kChunk = kXyMaxRounds - 2;
+        if ((int)pl.round_bits.size() <= kXyMaxRounds) {
+            plans.push_back(pl);
+            continue;
+        }
+        for (size_t r0 = 0; r0 < pl.round_bits.size(); r0 += kChunk) {
+            XyPassPlan part;
+            part.tile = pl.tile;
+            const size_t r1 = std::min(pl.round_bits.size(), r0 + kChunk);
+            part.round_bits.assign(pl.round_bits.begin() + r0, pl.round_bits.begin() + r1);
+            part.round_gates.assign(pl.round_gates.begin() + r0, pl.round_gates.begin() + r1);
+            if (!low_ok(part.round_bits.front())) {
+                part.round_bits.insert(part.round_bits.begin(), top);
+                part.round_gates.insert(part.round_gates.begin(), std::vector<std::pair<int, int>>());
+            }
+            if (!low_ok(part.round_bits.back())) {
+                part.round_bits.push_back(top);
+                part.round_gates.push_back({});
+            }
+            plans.push_back(part);
+        }
+    }
+    return plans;
+}
+
+static void fill_round(XyRound &R, const std::vector<int> &bits, const std::vector<std::pair<int, int>> &gl,
+                       const std::vector<int> &tile) {
+    std::memset(&R, 0, sizeof R);
+    for (int j = 0; j < 4; ++j) R.reg[j] = (unsigned char)bits[j];
+    // thread bits: the other 8 tile bits; the three lane bits of a quarter-warp get
+    // distinct residues mod 3 when possible (conflict-free swizzled smem), the rest ascending
+    std::vector<int> rest;
+    for (int b = 0; b < kTileBits; ++b)
+        if (std::find(bits.begin(), bits.end(), b) == bits.end()) rest.push_back(b);
+    std::vector<int> order;
+    bool low_lanes = true;  // keep lanes 0..4 on tile bits 0..4 when they are all thread bits (global access)
+    for (int b = 0; b < 5; ++b) low_lanes &= std::find(rest.begin(), rest.end(), b) != rest.end();
+    if (low_lanes) {
+        order = rest;
+    } else {
+        std::vector<int> pool = rest;
+        for (int res = 0; res < 3; ++res) {
+            auto it = std::find_if(pool.begin(), pool.end(), [&](int b) { return b % 3 == res; });
+            if (it != pool.end()) {
+                order.push_back(*it);
+                pool.erase(it);
+            }
+        }
+        for (int b : pool) order.push_back(b);
+    }
+    for (int k = 0; k < 8; ++k) R.tb[k] = (unsigned char)order[k];
+    for (int i = 0; i < kRegs; ++i) {
+        int e = 0;
+        for (int j = 0; j < 4; ++j)
+            if ((i >> j) & 1) e |= 1 << bits[j];
+        R.sreg[i] = (unsigned short)xy_slot(e);
+    }
+    R.ngates = (unsigned char)gl.size();
+    for (size_t g = 0; g < gl.size(); ++g) {
+        const int lo = std::min(gl[g].first, gl[g].second), hi = std::max(gl[g].first, gl[g].second);
+        const int tlo_bit = (int)(std::find(tile.begin(), tile.end(), lo) - tile.begin());
+        const int thi_bit = (int)(std::find(tile.begin(), tile.end(), hi) - tile.begin());
+        const int a = (int)(std::find(bits.begin(), bits.end(), tlo_bit) - bits.begin());
+        const int b = (int)(std::find(bits.begin(), bits.end(), thi_bit) - bits.begin());
+        R.gate[g] = (unsigned char)(4 * a + b);
+    }
+}
+
+template <int COST, int PH>
+static int launch_xy(const XyParams &P, int grid, cudaStream_t st) {
+    static bool configured = false;
+    const size_t smem = (size_t)(kTile + (kTableLo + kMaxTableHi) * kCopies) * sizeof(double2);
+    if (!configured) {
+        cudaFuncSetAttribute(k_xy_pass<COST, PH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    const size_t need = (size_t)(kTile + (PH && COST == FQ_COST_U16 ? (kTableLo + P.table_hi) * kCopies : 0)) *
+                        sizeof(double2);
+    k_xy_pass<COST, PH><<<grid, kThreads, need, st>>>(P);
+    FQ_LAUNCHED("k_xy_pass");
+    return FQ_OK;
+}
+
+// Whole XY program (n >= 13): p x (phase, gate sequence), expectation.
+int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>> &gates, cudaStream_t st,
+                 int *passes_out) {
+    const int n = d->n;
+    const long long size = 1LL << n;
+    double2 *psi = static_cast<double2 *>(d->psi);
+    const auto plans = plan_xy(n, gates);
+    for (auto &pl : plans)
+        if ((int)pl.round_bits.size() > kXyMaxRounds) {
+            set_error("run_xy_tiled: a pass needs %d register rounds (max %d)", (int)pl.round_bits.size(),
+                      kXyMaxRounds);
+            return FQ_ERR_UNSUPPORTED;
+        }
+    if (passes_out) *passes_out = (int)plans.size() * d->n_layers;
+    int table_hi = 0;
+    if (d->cost_kind == FQ_COST_U16 && d->cost_levels > 0) {
+        const int rows = ((d->cost_levels - 1) >> 6) + 1;
+        table_hi = rows <= kMaxTableHi ? rows : 0;
+    }
+    const int sms = sm_count() > 0 ? sm_count() : 148;
+    const long long n_tiles = 1LL << (n - kTileBits);
+    const int grid = (int)std::min<long long>(n_tiles, (long long)sms * 2);
+    bool init_pending = d->init != 0;
+    XyParams *P = new XyParams;
+    for (int l = 0; l < d->n_layers; ++l) {
+        const fq_layer &L = d->layers[l];
+        for (size_t pi = 0; pi < plans.size(); ++pi) {
+            const XyPassPlan &pl = plans[pi];
+            std::memset(P, 0, sizeof *P);
+            P->psi = psi;
+            P->costs = d->costs;
+            P->cost_scale = d->cost_scale;
+            P->cost_offset = d->cost_offset;
+            P->partials = d->scratch;
+            P->init_amp = d->init_amp;
+            P->gamma = L.gamma;
+            P->c = std::cos(L.beta);
+            P->s = std::sin(L.beta);
+            P->n_tiles = n_tiles;
+            for (int i = 0; i < kTileBits; ++i) P->tile_pos[i] = pl.tile[i];
+            P->init = init_pending ? 1 : 0;
+            init_pending = false;
+            P->expect = (l + 1 == d->n_layers && pi + 1 == plans.size() && d->expectation_dev) ? 1 : 0;
+            P->table_hi = table_hi;
+            P->nrounds = (int)pl.round_bits.size();
+            for (int r = 0; r < P->nrounds; ++r) fill_round(P->rounds[r], pl.round_bits[r], pl.round_gates[r], pl.tile);
+            for (int i = 0; i < kRegs; ++i) {
+                long long a = 0, b = 0;
+                for (int j = 0; j < 4; ++j)
+                    if ((i >> j) & 1) {
+                        a += 1LL << pl.tile[P->rounds[0].reg[j]];
+                        b += 1LL << pl.tile[P->rounds[P->nrounds - 1].reg[j]];
+                    }
+                P->roff_first[i] = a;
+                P->roff_last[i] = b;
+            }
+            const bool ph = pi == 0 && L.apply_phase && L.gamma != 0.0;
+            int s;
+            if (d->cost_kind == FQ_COST_U16) s = ph ? launch_xy<FQ_COST_U16, 1>(*P, grid, st) : launch_xy<FQ_COST_U16, 0>(*P, grid, st);
+            else s = ph ? launch_xy<FQ_COST_F64, 1>(*P, grid, st) : launch_xy<FQ_COST_F64, 0>(*P, grid, st);
+            if (s) {
+                delete P;
+                return s;
+            }
+            if (P->expect) {
+                k_sum_partials<<<1, 32, 0, st>>>(d->scratch, grid, d->expectation_dev);
+                FQ_LAUNCHED("k_sum_partials");
+            }
+        }
+    }
+    delete P;
+    if (init_pending) {  // zero layers
+        int s = fq_init_state(psi, size, -1, d->init_amp, 0, st);
+        if (s) return s;
+    }
+    if (d->n_layers == 0 && d->expectation_dev)
+        return fq_expectation(psi, d->costs, d->cost_kind, d->cost_scale, d->cost_offset, size, d->expectation_dev,
+                              d->scratch, st);
+    return FQ_OK;
+}
+
+int plan_xy_passes(int n, const std::vector<std::pair<int, int>> &gates) { return (int)plan_xy(n, gates).size(); }
+
+}  // namespace fq

@@ -88,14 +88,33 @@ _COST_MEMO: "OrderedDict[TermPolynomial, DeviceCosts]" = OrderedDict()
 _MEMO_SIZE = 32
 
 
+def _device_costs_for(poly: TermPolynomial) -> DeviceCosts:
+    """Diagonal of a polynomial sized for one state of the same n next to it:
+    float64 + uint16 levels when 26 B/amplitude fit, else (integer / dyadic
+    weights, e.g. LABS n = 33 on one B200) the uint16 levels alone, computed
+    exactly from the terms — the reference's n <= 30 cap (terms.py:109-113)
+    becomes this device-memory check."""
+    free, _ = torch.cuda.mem_get_info(_lib.device())
+    size = 1 << poly.n
+    if size * (16 + 8 + 2) <= 0.95 * free:
+        return DeviceCosts.from_polynomial(poly)
+    if size * (16 + 2) <= 0.95 * free:
+        try:
+            return DeviceCosts.from_polynomial(poly, keep_f64=False)
+        except MemoryError:
+            pass
+    _check_fits(poly.n, 16 + 8, "state vector + cost vector")
+    return DeviceCosts.from_polynomial(poly)
+
+
 def _cached_device_costs(poly: TermPolynomial) -> DeviceCosts:
     """Process-wide memo of device diagonals (reference qaoa.py:71-75, lru 32)."""
     dc = _COST_MEMO.get(poly)
     if dc is not None:
         _COST_MEMO.move_to_end(poly)
         return dc
-    _check_fits(poly.n, 8, "cost vector")
-    dc = DeviceCosts.from_polynomial(poly)
+    _check_fits(poly.n, 2, "cost vector")
+    dc = _device_costs_for(poly)
     instrumentation.bump("precompute")
     _COST_MEMO[poly] = dc
     while len(_COST_MEMO) > _MEMO_SIZE:
@@ -114,8 +133,9 @@ def resolve_costs(problem) -> tuple[DeviceCosts, int]:
     return dc, dc.n
 
 
-def _initial_state(n: int, mixer: Mixer, initial) -> tuple[torch.Tensor, bool]:
-    """(device state, generate-|+>-in-kernel flag) — reference qaoa.py:90-103."""
+def _initial_state(n: int, mixer: Mixer, initial, out: torch.Tensor | None = None) -> tuple[torch.Tensor, bool]:
+    """(device state, generate-|+>-in-kernel flag) — reference qaoa.py:90-103.
+    ``out``: caller-owned buffer the |+> program evolves into (no allocation)."""
     dev = _lib.device()
     if initial is not None:
         if isinstance(initial, torch.Tensor):
@@ -131,6 +151,8 @@ def _initial_state(n: int, mixer: Mixer, initial) -> tuple[torch.Tensor, bool]:
             "XY mixers act within a fixed-popcount sector; pass an initial "
             "state explicitly (see statevec.hamming_weight_state)"
         )
+    if out is not None:
+        return out, True
     try:
         return torch.empty(1 << n, dtype=torch.complex128, device=dev), True
     except torch.OutOfMemoryError as exc:
@@ -140,9 +162,7 @@ def _initial_state(n: int, mixer: Mixer, initial) -> tuple[torch.Tensor, bool]:
 
 def _evolve(dc: DeviceCosts, n: int, mixer: Mixer, params: QaoaParams, initial,
             out: torch.Tensor | None = None) -> QaoaResult:
-    state, init = _initial_state(n, mixer, initial)
-    if out is not None and init:
-        state = out
+    state, init = _initial_state(n, mixer, initial, out=out)
     layers = [(g, b, 1, 0, n) for g, b in zip(params.gammas, params.betas)]
     exp_dev = torch.empty(1, dtype=torch.float64, device=state.device)
     run_program(state, n, mixer.kind, layers, dc=dc, su2=mixer.su2_table(params.betas, n),
@@ -162,8 +182,8 @@ class QaoaSimulator:
                 if n is None:
                     raise ValueError("a plain term list needs n")
                 terms = TermPolynomial.from_pairs(n, terms)
-            _check_fits(terms.n, 8, "cost vector")
-            self._dc = DeviceCosts.from_polynomial(terms)
+            _check_fits(terms.n, 2, "cost vector")
+            self._dc = _device_costs_for(terms)
             instrumentation.bump("precompute")
             self.n = terms.n
         else:

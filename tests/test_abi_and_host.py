@@ -160,3 +160,21 @@ def test_graph_validation():
              if not l.startswith("#")]
     g = Graph.from_edges(26, edges)
     assert len(g.edges) == 39 and len(maxcut_terms(g).terms) == 40
+
+
+def test_xy_planner_and_host_program_without_gpu():
+    """The tiled-XY scheduler and the whole host side of fq_qaoa_evolve run on
+    CPU up to the first launch (which must fail cleanly: no device)."""
+    import ctypes
+
+    lib = _lib.load()
+    assert lib.fq_plan_xy_passes(12, 1) == 1  # on chip
+    assert lib.fq_plan_xy_passes(26, 1) <= 5  # ring: 26 gates in a handful of passes
+    assert lib.fq_plan_xy_passes(26, 2) <= 40  # complete: 325 gates
+    for n in (13, 20, 26):
+        for mixer in (1, 2):
+            lay = (_lib.FqLayer * 2)(_lib.FqLayer(0.1, 0.2, 1, 0, n), _lib.FqLayer(0.3, 0.4, 1, 0, n))
+            d = _lib.FqEvolveDesc()
+            d.psi, d.n, d.cost_kind, d.costs, d.mixer = 0x1000, n, 0, 0x2000, mixer
+            d.n_layers, d.layers, d.scratch = 2, lay, 0x3000
+            assert lib.fq_qaoa_evolve(ctypes.byref(d), None) == _lib.FQ_ERR_CUDA

@@ -124,7 +124,7 @@ def test_custom_mixer_random_su2_vs_oracle(n, pass_plan):
 
 
 @pytest.mark.parametrize("kind", ["xy-ring", "xy-complete"])
-@pytest.mark.parametrize("n", [6, 13, 14])
+@pytest.mark.parametrize("n", [6, 13, 14, 17, 20])
 def test_xy_mixers_vs_oracle(kind, n):
     rng = np.random.default_rng(n)
     p = 2
@@ -138,6 +138,32 @@ def test_xy_mixers_vs_oracle(kind, n):
     np.testing.assert_allclose(res.state, ref, rtol=0, atol=1e-12)
     w = np.bitwise_count(np.arange(1 << n, dtype=np.uint64))
     assert np.sum(np.abs(res.state[w != n // 2]) ** 2) < 1e-20
+
+
+@pytest.mark.parametrize("kind", ["xy-ring", "xy-complete"])
+@pytest.mark.parametrize("n,p", [(13, 1), (16, 2), (19, 1), (22, 1)])
+def test_tiled_xy_random_state_and_per_gate_path(kind, n, p):
+    """Tiled XY passes (gate-sequence scheduler, register rounds, swizzled
+    transposes) on a random complex initial state with float64 costs, against
+    the oracle and against the one-kernel-per-gate path (option xy_tiled=0)."""
+    from paper_2309_04841_b200 import _lib
+
+    rng = np.random.default_rng(100 + n)
+    g, b = rng.uniform(-1, 1, p), rng.uniform(-1.6, 1.6, p)
+    init = random_state(rng, n)
+    poly = TermPolynomial.from_pairs(n, random_pairs(rng, n, max_terms=2 * n))
+    sim = QaoaSimulator(terms=poly, mixer=kind)
+    res = sim.simulate_qaoa(g, b, initial=init)
+    costs = sim.get_cost_diagonal()
+    ref = O.simulate(costs, g, b, kind, np.array(init))
+    np.testing.assert_allclose(res.state, ref, rtol=0, atol=1e-12)
+    assert sim.get_expectation(res) == pytest.approx(O.expectation(ref, costs), rel=1e-10, abs=1e-12)
+    _lib.call("fq_set_option", b"xy_tiled", 0)
+    try:
+        res0 = sim.simulate_qaoa(g, b, initial=init)
+    finally:
+        _lib.call("fq_set_option", b"xy_tiled", 1)
+    np.testing.assert_allclose(res.state, res0.state, rtol=0, atol=1e-12)
 
 
 def test_batched_small_n_matches_single():
