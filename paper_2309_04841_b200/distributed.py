@@ -379,8 +379,10 @@ class ShardedQaoaSimulator:
         params = QaoaParams(tuple(gammas), tuple(betas))
         if self.mixer.preserves_hamming_weight and initial_weight is None:
             raise ValueError("XY mixers need initial_weight (Hamming-weight sector)")
-        if self.mixer.kind != "x":
-            raise NotImplementedError("multi-process sharding supports the X mixer (XY: simulate_qaoa_distributed)")
+        if self.mixer.kind == "custom":
+            raise NotImplementedError("multi-process sharding supports the X and XY mixers")
+        if self.mixer.preserves_hamming_weight:
+            return self._simulate_xy(params, initial_weight, expectation)
         nl, k = self.n_local, self.k
         psi = self.ops.empty(nl) if initial_weight is None else self.initial_state(initial_weight)
         init = initial_weight is None
@@ -397,6 +399,47 @@ class ShardedQaoaSimulator:
         if not expectation:
             return None
         return self.expectation()
+
+    # ------------------------------------------------------------------ XY mixers
+    def _xy_gate(self, psi: torch.Tensor, beta: float, i: int, j: int) -> torch.Tensor:
+        """One XY gate on the sharded state (reference distributed.py:160-207):
+        local pairs directly; a pair touching a global qubit inside an
+        exchange pair, a subchunk-id partner parked at local position 0."""
+        n, k, nl = self.n, self.k, self.n_local
+        lo, hi = min(i, j), max(i, j)
+        if hi < nl:
+            self.ops.xy(psi, beta, lo, hi)
+            return psi
+        b_start = n - 2 * k
+        parked = False
+        if b_start <= lo < nl:
+            if b_start == 0:
+                raise ValueError(
+                    f"pair ({i}, {j}) spans the subchunk-id and worker-id qubits; "
+                    f"with 2*log2(K) == n there is no local position to stage it (use fewer workers)"
+                )
+            self.ops.swap(psi, 0, lo)
+            lo, parked = 0, True
+        pos_lo = lo - k if lo >= nl else lo
+        pos_hi = hi - k
+        psi = self.exchange(psi)
+        self.ops.xy(psi, beta, min(pos_lo, pos_hi), max(pos_lo, pos_hi))
+        psi = self.exchange(psi)
+        if parked:
+            self.ops.swap(psi, 0, min(i, j))
+        return psi
+
+    def _simulate_xy(self, params: QaoaParams, initial_weight: int, expectation: bool):
+        nl = self.n_local
+        edges = ring_edges(self.n) if self.mixer.kind == "xy-ring" else complete_edges(self.n)
+        psi = self.initial_state(initial_weight)
+        for g, b in zip(params.gammas, params.betas):
+            if g != 0.0:
+                self.ops.program(psi, nl, "x", [(g, 0.0, 1, 0, 0)], self.costs)
+            for i, j in edges:
+                psi = self._xy_gate(psi, b, i, j)
+        self._state = psi
+        return self.expectation() if expectation else None
 
     def expectation(self) -> float:
         local = self.ops.expectation(self._state, self.costs)
@@ -447,6 +490,13 @@ class CudaLocalOps:
 
     def program(self, psi, n_local, kind, layers, costs, init=False, init_amp=0.0):
         run_program(psi, n_local, kind, layers, dc=costs, init=init, init_amp=init_amp)
+
+    def xy(self, psi, beta, lo, hi):
+        _lib.call("fq_xy_on_pairs", psi.data_ptr(), psi.numel(), float(np.cos(beta)), float(np.sin(beta)), lo, hi,
+                  _lib.stream())
+
+    def swap(self, psi, lo, hi):
+        _lib.call("fq_swap_bits", psi.data_ptr(), psi.numel(), lo, hi, _lib.stream())
 
     def expectation(self, psi, costs) -> torch.Tensor:
         return expectation_device(psi, costs)

@@ -54,6 +54,12 @@ class OracleOps:
             for q in range(lo, hi):
                 O.su2_on_pairs(st, a, bb, q)
 
+    def xy(self, psi, beta, lo, hi):
+        O.xy_on_pairs(psi.numpy(), float(np.cos(beta)), float(np.sin(beta)), lo, hi)
+
+    def swap(self, psi, lo, hi):
+        O.swap_bits(psi.numpy(), lo, hi)
+
     def expectation(self, psi, costs):
         return torch.tensor([O.expectation(psi.numpy(), costs)], dtype=torch.float64)
 
@@ -118,3 +124,51 @@ def test_sharded_world2_matches_single_node(n, p, chunk):
         assert ov == pytest.approx(ov_ref, abs=1e-12)
         assert ex == 2 * p and ex_counter == 2 * p  # Alg. 4: two exchanges per X layer
     np.testing.assert_allclose(out[0][5], ref, rtol=0, atol=1e-12)
+
+
+def _xy_worker(rank, world, port, n, p, kind, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2309_04841_b200.distributed import ShardedQaoaSimulator
+        from paper_2309_04841_b200.problems import portfolio_terms
+
+        rng = np.random.default_rng(7)
+        g, b = rng.uniform(-1, 1, p), rng.uniform(-1, 1, p)
+        sim = ShardedQaoaSimulator(portfolio_terms(n), mixer=kind, local_ops=OracleOps())
+        E = sim.simulate_qaoa(g, b, initial_weight=n // 2)
+        shards = [torch.empty_like(sim.shard) for _ in range(world)]
+        dist.all_gather(shards, sim.shard)
+        q.put((rank, E, sim.exchange_count, torch.cat(shards).numpy() if rank == 0 else None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["xy-ring", "xy-complete"])
+def test_sharded_xy_world2_matches_single_node(kind):
+    """XY mixers over 2 ranks (reference distributed.py:160-207 algorithm: park +
+    exchange for pairs touching the global qubit) equal the single-node oracle."""
+    n, p, world = 8, 2, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xy_worker, args=(r, world, port, n, p, kind, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    rng = np.random.default_rng(7)
+    g, b = rng.uniform(-1, 1, p), rng.uniform(-1, 1, p)
+    from paper_2309_04841_b200.problems import portfolio_terms
+
+    poly = portfolio_terms(n)
+    costs = O.precompute_cost_vector(n, [(t.weight, t.support) for t in poly.terms])
+    ref = O.simulate(costs, g, b, kind, O.hamming_weight_state(n, n // 2))
+    edges = O.ring_edges(n) if kind == "xy-ring" else O.complete_edges(n)
+    assert out[0][2] == p * 2 * sum(1 for i, j in edges if max(i, j) >= n - 1)  # 2 exchanges per global pair
+    for rank, E, ex, state in out:
+        assert E == pytest.approx(O.expectation(ref, costs), rel=1e-12, abs=1e-12)
+    np.testing.assert_allclose(out[0][3], ref, rtol=0, atol=1e-12)
