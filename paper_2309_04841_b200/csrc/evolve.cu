@@ -422,6 +422,17 @@ static int build_tile_map(CUtensorMap *map, const void *gaddr, int n, const int 
     return r == CUDA_SUCCESS ? rank : 0;
 }
 
+// pdep: the bits of x into the positions NOT set in mask (ascending)
+static long long deposit(long long x, long long mask) {
+    long long out = 0;
+    for (int b = 0; b < 63 && x; ++b) {
+        if ((mask >> b) & 1) continue;
+        if (x & 1) out |= 1LL << b;
+        x >>= 1;
+    }
+    return out;
+}
+
 // Mask class of a pass (template K of k_pass16) from its per-round masks.
 static int mask_class(int seq, const unsigned char *maskA) {
     const int nr = seq_rounds(seq);
@@ -536,7 +547,8 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
                 long long o = 0;
                 for (int j = 0; j < 4; ++j)
                     if ((i >> j) & 1) o += 1LL << g.tile_pos[f + j];
-                P.roff[pat][i] = o;
+                P.roff[pat][i] = o * (long long)sizeof(double2);
+                P.coff[pat][i] = o * (d->cost_kind == FQ_COST_F64 ? 8 : 2);
             }
         }
         P.init = init_pending ? 1 : 0;
@@ -571,6 +583,9 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
         fill(pp.layerA, P.A);
         if (two) fill(pp.layerB, P.B);
         P.final_scale = fscale;
+        P.tile_mask = 0;
+        for (int i = 0; i < kTileBits; ++i) P.tile_mask |= 1LL << g.tile_pos[i];
+        P.step_dep = deposit(grid, P.tile_mask);
         P.pf_dist = g_prefetch;
         P.probe = g_probe;
         P.run_bits = 0;

@@ -68,8 +68,11 @@ struct PassParams {
     int sm_rank, sm_shift[5], sm_bits[5];  // state tensor map: rank, outer-dim coordinate = (t >> shift) & (2^bits - 1)
     int cm_rank, cm_shift[5], cm_bits[5];  // cost tensor map (cm_rank = 0: no cost prefetch)
     int probe;                // development: 1 no cost loads, 2 fixed table row, 4 no phase multiply
-    long long roff[3][kRegs]; // per pattern: physical offset of register i (read from the constant bank,
-                              // so no register holds the 16 offsets across the rounds)
+    long long roff[3][kRegs]; // per pattern: BYTE offset of register i in the state (read from the constant
+                              // bank, so no register holds the 16 offsets across the rounds)
+    long long coff[3][kRegs]; // the same in the cost vector (bytes)
+    long long tile_mask;      // bits at the tile positions
+    long long step_dep;       // pdep(gridDim.x) into the non-tile positions: base(t + grid) = next_base(base(t))
     CoefSet A, B;
 };
 
@@ -205,6 +208,12 @@ __device__ __forceinline__ CostRaw<COST> load_cost(const PassParams &P, long lon
 }
 
 template <int COST>
+__device__ __forceinline__ CostRaw<COST> load_cost_at(const char *p) {
+    if constexpr (COST == FQ_COST_F64) return __ldcs(reinterpret_cast<const double *>(p));
+    else return (unsigned)__ldcs(reinterpret_cast<const unsigned short *>(p));
+}
+
+template <int COST>
 __device__ __forceinline__ double decode_cost(const PassParams &P, CostRaw<COST> raw) {
     if constexpr (COST == FQ_COST_F64) return raw;
     else return decode_u16((uint16_t)raw, P.cost_scale, P.cost_offset);
@@ -247,6 +256,12 @@ __device__ __forceinline__ long long tile_base(const PassParams &P, long long t)
         base = ((base >> p) << (p + 1)) | (base & ((1LL << p) - 1));
     }
     return base;
+}
+
+// Tile bases advance in "deposited" space: adding Y = pdep(stride) with the
+// tile-bit positions pre-filled with ones lets carries hop over them.
+__device__ __forceinline__ long long next_base(long long base, long long mask, long long y) {
+    return ((base | mask) + y) & ~mask;
 }
 
 // L2 prefetch of a future tile with ONE instruction: the tile is described
@@ -356,36 +371,38 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
             if (tp < P.n_tiles) prefetch_tile(P, &tm_state, &tm_cost, tp, !P.init);
         }
     }
-    for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
-        const long long base = tile_base(P, t);
+    constexpr int CB = COST == FQ_COST_F64 ? 8 : 2;
+    long long base = tile_base(P, blockIdx.x);
+    for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x, base = next_base(base, P.tile_mask, P.step_dep)) {
         if (pf) {
             const long long tp = t + (long long)P.pf_dist * gridDim.x;
             if (tp < P.n_tiles) prefetch_tile(P, &tm_state, &tm_cost, tp, !P.init);
         }
+        // per-tile base pointers; the registers' offsets are constant-bank byte offsets
+        const char *ps8 = reinterpret_cast<const char *>(P.psi + base + thr8);
+        const char *cs = static_cast<const char *>(P.costs) + base * CB;
         double2 v[kRegs];
         CostRaw<COST> raw[kRegs];  // cost entries of the phase round, loaded with the state
-        {
-            const long long *o = P.roff[PAT8];
-            if (P.init) {
+        if (P.init) {
 #pragma unroll
-                for (int i = 0; i < kRegs; ++i) v[i] = make_double2(P.init_amp, 0.0);
-            } else {
+            for (int i = 0; i < kRegs; ++i) v[i] = make_double2(P.init_amp, 0.0);
+        } else {
 #pragma unroll
-                for (int i = 0; i < kRegs; ++i) v[i] = ld_stream(P.psi + base + thr8 + o[i]);
-            }
-            if (PH == 1) {
+            for (int i = 0; i < kRegs; ++i) v[i] = ld_stream(reinterpret_cast<const double2 *>(ps8 + P.roff[PAT8][i]));
+        }
+        if (PH == 1) {
+            const char *c8 = cs + thr8 * CB;
 #pragma unroll
-                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost<COST>(P, base + thr8 + o[i]);
-            }
+            for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c8 + P.coff[PAT8][i]);
         }
         if (PH == 2) {
-            const long long *o = P.roff[PAT4];
             if (P.probe & 1) {
 #pragma unroll
                 for (int i = 0; i < kRegs; ++i) raw[i] = (CostRaw<COST>)((tid * 7 + i * 131) & 1023);
             } else {
+                const char *c4 = cs + thr4 * CB;
 #pragma unroll
-                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost<COST>(P, base + thr4 + o[i]);
+                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c4 + P.coff[PAT4][i]);
             }
         }
         auto phase_all = [&]() {
@@ -437,18 +454,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
             bfly16<MIX, MB, PAT8>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
         }
         // ---- store (+ expectation) in the last round's pattern
-        const long long *o = P.roff[LAST];
         const double fs = P.final_scale;
         if (P.expect) {  // cost entries of the last pattern (only the program's final pass)
+            const char *cl = cs + thrL * CB;
 #pragma unroll
-            for (int i = 0; i < kRegs; ++i) raw[i] = load_cost<COST>(P, base + thrL + o[i]);
+            for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i]);
         }
+        char *psl = reinterpret_cast<char *>(P.psi + base + thrL);
 #pragma unroll
         for (int i = 0; i < kRegs; ++i) {
             double2 x = v[i];
             if (MIX == MIX_RX) x = make_double2(x.x * fs, x.y * fs);
             if (P.expect) eacc += decode_cost<COST>(P, raw[i]) * (x.x * x.x + x.y * x.y);
-            st_stream(P.psi + base + thrL + o[i], x);
+            st_stream(reinterpret_cast<double2 *>(psl + P.roff[LAST][i]), x);
         }
     }
     if (P.expect) {

@@ -347,7 +347,7 @@ class ShardedQaoaSimulator:
         if full_ok:
             if self._spare is None or self._spare.numel() != shard.numel():
                 self._spare = torch.empty_like(shard)
-            dist.all_to_all_single(self._spare, shard, group=self.group)
+            self._a2a(self._spare, shard)
             out, self._spare = self._spare, shard
         else:
             # bounded staging: column block [c0, c1) of every subchunk per round;
@@ -360,12 +360,22 @@ class ShardedQaoaSimulator:
                 c1 = min(sub, c0 + piece)
                 send = V[:, c0:c1].contiguous()
                 recv = torch.empty_like(send)
-                dist.all_to_all_single(recv, send, group=self.group)
+                self._a2a(recv, send)
                 V[:, c0:c1].copy_(recv)
             out = shard
         self.exchange_count += 1
         instrumentation.bump("exchange")
         return out
+
+    def _a2a(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        """all_to_all_single; over a CPU-only backend (gloo) CUDA shards are
+        staged through host memory (NCCL moves them GPU to GPU over NVLink)."""
+        if inp.is_cuda and dist.get_backend(self.group) == "gloo":
+            host = torch.empty_like(inp, device="cpu")
+            dist.all_to_all_single(host, inp.cpu(), group=self.group)
+            out.copy_(host)
+        else:
+            dist.all_to_all_single(out, inp, group=self.group)
 
     # ------------------------------------------------------------------ evolution
     def initial_state(self, initial_weight: int | None = None) -> torch.Tensor:
