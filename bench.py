@@ -305,7 +305,7 @@ def main():
             for i in range(cnt):
                 sq, ph, nt, ini, ex = info[5 * i:5 * i + 5]
                 nb = (0 if ini else S) + S + (Cb if (ph or ex) else 0)
-                kd = kinds.setdefault(PASS_NAMES.get(sq, str(sq)) + (" +phase" if ph else "") +
+                kd = kinds.setdefault(PASS_NAMES.get(sq, str(sq)) + (" +phase" if ph in (1, 2) else "") +
                                       (" +init" if ini else "") + (" +expect" if ex else ""),
                                       {"launches": 0, "ms": 0.0, "bytes": 0})
                 kd["launches"] += 1

@@ -605,6 +605,7 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
             if (P.sm_rank == 0 && P.cm_rank == 0) P.pf_dist = 0;
         }
         const int ma = P.A.mode, mb = two ? P.B.mode : 2;
+        if (P.expect && ph == 0 && !two && !seq_heavy(sq)) ph = 3;  // preload the expectation's costs
         const int s = launch_pass(mix, d->cost_kind, P, M, sq, ph, ma, mb, grid, st);
         if (s) return s;
         g_last_plan.push_back({sq, ph, (int)g.targets.size(), P.init, P.expect});

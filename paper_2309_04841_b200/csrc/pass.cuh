@@ -332,7 +332,8 @@ __device__ __forceinline__ int round_mask(const unsigned char *rt, int r) {
 // on it:
 //   SEQ: round program (see SEQ_*);
 //   PH: 0 no phase, 1 phase before set A in round 0, 2 phase between set A and
-//       set B in the middle (PAT4) round of a heavy SEQ;
+//       set B in the middle (PAT4) round of a heavy SEQ, 3 no phase and the
+//       expectation's costs loaded with the state (the program's last pass);
 //   MA, MB: RX form of sets A/B (0: (1, tan b), 1: (cot b, 1), 3: chosen at run
 //       time); MB = 2: no set B;
 //   K: target-mask class of the rounds (see round_mask): compile-time masks keep
@@ -352,10 +353,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
     constexpr bool HEAVY = seq_heavy(SEQ);
     static_assert(!HEAVY || (PH == 2 && HAS_B), "heavy round programs carry the mid-layer phase");
     static_assert(HEAVY || PH != 2, "the mid-layer phase needs a heavy round program");
+    static_assert(!HEAVY || PH != 3, "PH = 3 (expectation preload) is a light-pass mode");
     constexpr int NR = seq_rounds(SEQ);
     constexpr int LAST = seq_pat(SEQ, NR - 1);
 
-    if (COST == FQ_COST_U16 && PH != 0) {
+    if (COST == FQ_COST_U16 && (PH == 1 || PH == 2)) {
         if (P.table_hi > 0) build_phase_tables(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
         __syncthreads();
     }
@@ -394,6 +396,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
             const char *c8 = cs + thr8 * CB;
 #pragma unroll
             for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c8 + P.coff[PAT8][i]);
+        }
+        if (PH == 3) {  // the program's last pass: its expectation costs, in the store pattern
+            const char *cl = cs + thrL * CB;
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i]);
         }
         if (PH == 2) {
             if (P.probe & 1) {
@@ -455,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
         }
         // ---- store (+ expectation) in the last round's pattern
         const double fs = P.final_scale;
-        if (P.expect) {  // cost entries of the last pattern (only the program's final pass)
+        if (PH != 3 && P.expect) {  // cost entries of the last pattern (final pass with a phase)
             const char *cl = cs + thrL * CB;
 #pragma unroll
             for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i]);
@@ -520,8 +527,8 @@ static int select_seq(const PassParams &P, const PassMaps &M, int ph, int ma, in
             FQ_K(2, 0, 3)
         }
     } else {
-        FQ_K(0, 0, 2) FQ_K(0, 0, 3) FQ_K(1, 0, 2) FQ_K(1, 0, 3)
-        if constexpr (MIX == MIX_RX) { FQ_K(0, 1, 2) FQ_K(0, 1, 3) FQ_K(1, 1, 2) FQ_K(1, 1, 3) }
+        FQ_K(0, 0, 2) FQ_K(0, 0, 3) FQ_K(1, 0, 2) FQ_K(1, 0, 3) FQ_K(3, 0, 2)
+        if constexpr (MIX == MIX_RX) { FQ_K(0, 1, 2) FQ_K(0, 1, 3) FQ_K(1, 1, 2) FQ_K(1, 1, 3) FQ_K(3, 1, 2) }
     }
 #undef FQ_K
     set_error("k_pass16: no instantiation for seq=%d ph=%d ma=%d mb=%d", SEQ, ph, ma, mb);
