@@ -187,6 +187,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="total qubits (default 26 + log2 N)")
     ap.add_argument("--p", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--global-mode", default="p2p", choices=["p2p", "exchange"],
+                    help="N>1: global-qubit mixer as one peer-memory kernel (p2p) or NCCL all-to-all exchanges")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -227,7 +229,7 @@ def main():
         sim = QaoaSimulator(terms=poly)
         dc = sim.device_costs
     else:
-        sim = ShardedQaoaSimulator(poly)
+        sim = ShardedQaoaSimulator(poly, global_mode=args.global_mode)
         dc = sim.costs
     barrier()
     precompute_s = time.perf_counter() - t0
@@ -397,7 +399,9 @@ def main():
                        "n": n, "p": p, "n_local": n_local, "angles": "default_rng(0) U(0,1)",
                        "cost_encoding": "uint16 levels (lossless)" if dc.u16 is not None else "float64",
                        "l2": "no flush: 1 GiB state per GPU >> 126 MB L2",
-                       "parallelism": f"state sharded over {world} GPUs" if world > 1 else "single GPU"},
+                       "parallelism": (f"state sharded over {world} GPUs by global qubits, global-qubit mixer: "
+                                       f"{'peer-memory kernel (CUDA IPC over NVLink)' if args.global_mode == 'p2p' else 'NCCL all-to-all'}")
+                                      if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                          "kernel": "k_pass16 (every tiled pass of the step; per-launch CUDA events)",

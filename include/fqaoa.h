@@ -186,6 +186,26 @@ int fq_qaoa_evolve_batched(int n, int mixer, const void *costs, int cost_kind, d
  * byte model in bench.py / DESIGN.md). */
 int fq_plan_x_passes(int n, int n_layers, const fq_layer *layers);
 
+/* ------------------------------------------------------------------ *
+ * Sharded state over peer memory                                       *
+ * ------------------------------------------------------------------ */
+
+/* Fused global-qubit mixer (replaces the exchange -> k-position pass ->
+ * exchange of reference distributed.py:137-153 / Alg. 4): shards[r] (host
+ * array of 2^k device pointers, all shard_size amplitudes, peer-mapped) hold
+ * the state slice of global index r; applies su2[j] = (a_re, a_im, b_re, b_im)
+ * to global qubit j (bit j of r) for the local indices of part `part` of
+ * `parts` (each rank / worker passes its own part), in place.  The caller
+ * orders it against the other parts' work. */
+int fq_global_su2_pass(void *const *shards, int k, int64_t shard_size, int part, int parts, const double *su2,
+                       void *stream);
+
+/* CUDA IPC of a device buffer (any pointer inside a cudaMalloc allocation):
+ * 64-byte handle + offset; open maps it into this process (same or peer GPU). */
+int fq_ipc_handle(const void *dev_ptr, void *handle_out, int64_t *offset_out);
+int fq_ipc_open(const void *handle, int64_t offset, void **dev_ptr_out);
+int fq_ipc_close(void *dev_ptr, int64_t offset);
+
 /* HBM passes per layer of the tiled XY program (ring / complete gate order of
  * reference mixers.py:109-125) at n qubits; 1 for n <= 12 (on chip), -1 for other kinds. */
 int fq_plan_xy_passes(int n, int mixer);

@@ -278,10 +278,24 @@ class DistributedResult:
         return QaoaResult(state, self.costs_device)
 
 
+def global_su2_pass(shard_ptrs: Sequence[int], k: int, shard_size: int, part: int, parts: int,
+                    us: Sequence[SU2]) -> None:
+    """libfqaoa fq_global_su2_pass: u_j on global qubit j across the 2^k peer-mapped
+    shards, in place, for local indices of `part` of `parts`."""
+    import ctypes
+
+    ptrs = (ctypes.c_void_p * len(shard_ptrs))(*shard_ptrs)
+    coef = np.array([(complex(u.a).real, complex(u.a).imag, complex(u.b).real, complex(u.b).imag) for u in us],
+                    dtype=np.float64)
+    _lib.call("fq_global_su2_pass", ptrs, k, shard_size, part, parts, coef.ctypes.data, _lib.stream())
+
+
 def simulate_qaoa_distributed(problem, params: QaoaParams, K: int, mixer: "str | Mixer" = "x",
-                              initial=None) -> DistributedResult:
+                              initial=None, fused: bool = True) -> DistributedResult:
     """K logical workers on the current GPU (reference distributed.py:280-296).
-    For the X mixer, phase + local qubits run as one fused program per shard."""
+    For the X mixer, phase + local qubits run as one fused program per shard;
+    the global qubits run in one peer-memory pass over all shards (``fused``;
+    False = the reference's exchange -> pass -> exchange)."""
     dc, n = resolve_costs(problem)
     mixer = Mixer.parse(mixer)
     k = _validate_split(n, K)
@@ -295,6 +309,13 @@ def simulate_qaoa_distributed(problem, params: QaoaParams, K: int, mixer: "str |
         if mixer.kind == "x" and k > 0:
             for shard, c in zip(sharded.shards, sc.shards):
                 run_program(shard, n_local, "x", [(gamma, beta, 1, 0, n_local)], dc=c)
+            if fused and k <= 4:
+                # one peer-memory kernel replaces exchange -> k-position pass -> exchange;
+                # the two logical exchanges of Alg. 4 are still counted (reference API)
+                global_su2_pass([s.data_ptr() for s in sharded.shards], k, 1 << n_local, 0, 1, [SU2.rx(beta)] * k)
+                sharded.exchange_count += 2
+                instrumentation.bump("exchange", 2)
+                continue
             all_to_all_exchange(sharded)
             for shard in sharded.shards:
                 run_program(shard, n_local, "x", [(0.0, beta, 0, n_local - k, n_local)])
@@ -318,7 +339,7 @@ class ShardedQaoaSimulator:
 
     def __init__(self, poly: TermPolynomial, group=None, mixer: "str | Mixer" = "x",
                  compact: bool = True, keep_f64: bool | None = None, chunk_bytes: int | None = None,
-                 local_ops=None):
+                 local_ops=None, global_mode: str = "exchange"):
         self.group = group
         self.K = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -336,6 +357,12 @@ class ShardedQaoaSimulator:
         self.chunk_bytes = chunk_bytes
         self._state = None
         self._spare = None
+        if global_mode not in ("exchange", "p2p"):
+            raise ValueError(f"global_mode must be 'exchange' or 'p2p', got {global_mode!r}")
+        self.global_mode = global_mode
+        self._p2p_buf = None
+        self._peers: list[int] | None = None
+        self._opened: list[tuple[int, int]] = []
 
     # ------------------------------------------------------------------ exchange
     def exchange(self, shard: torch.Tensor) -> torch.Tensor:
@@ -394,12 +421,19 @@ class ShardedQaoaSimulator:
         if self.mixer.preserves_hamming_weight:
             return self._simulate_xy(params, initial_weight, expectation)
         nl, k = self.n_local, self.k
-        psi = self.ops.empty(nl) if initial_weight is None else self.initial_state(initial_weight)
+        if self.global_mode == "p2p" and k > 0:
+            psi = self._p2p_shard()
+            if initial_weight is not None:
+                psi.copy_(self.initial_state(initial_weight))
+        else:
+            psi = self.ops.empty(nl) if initial_weight is None else self.initial_state(initial_weight)
         init = initial_weight is None
         amp = 1.0 / sqrt(float(2 ** self.n)) if init else 0.0
         for li, (g, b) in enumerate(zip(params.gammas, params.betas)):
             self.ops.program(psi, nl, "x", [(g, b, 1, 0, nl)], self.costs, init=init and li == 0, init_amp=amp)
-            if k > 0:
+            if k > 0 and self.global_mode == "p2p":
+                self._global_p2p(b)
+            elif k > 0:
                 psi = self.exchange(psi)
                 self.ops.program(psi, nl, "x", [(0.0, b, 0, nl - k, nl)], None)
                 psi = self.exchange(psi)
@@ -409,6 +443,53 @@ class ShardedQaoaSimulator:
         if not expectation:
             return None
         return self.expectation()
+
+    # ------------------------------------------------------------------ peer-memory global pass
+    def _p2p_shard(self) -> torch.Tensor:
+        """Persistent shard buffer, mapped into every rank (CUDA IPC handles
+        all-gathered once).  NVLink peers on one node; on one device (tests)
+        the same IPC path maps another process's allocation."""
+        if self._p2p_buf is None:
+            import ctypes
+
+            self._p2p_buf = self.ops.empty(self.n_local)
+            h = (ctypes.c_char * 64)()
+            off = ctypes.c_int64()
+            _lib.call("fq_ipc_handle", self._p2p_buf.data_ptr(), h, ctypes.byref(off))
+            mine = (bytes(h), off.value)
+            allh = [None] * self.K
+            dist.all_gather_object(allh, mine, group=self.group)
+            peers = []
+            for r, (hb, o) in enumerate(allh):
+                if r == self.rank:
+                    peers.append(self._p2p_buf.data_ptr())
+                    continue
+                ptr = ctypes.c_void_p()
+                _lib.call("fq_ipc_open", hb, o, ctypes.byref(ptr))
+                peers.append(ptr.value)
+                self._opened.append((ptr.value, o))
+            self._peers = peers
+        return self._p2p_buf
+
+    def _global_p2p(self, beta: float) -> None:
+        """Alg. 4's exchange -> k-position pass -> exchange as ONE peer-memory
+        kernel per rank (fq_global_su2_pass): rank r transforms the local
+        indices of its 1/K part across all K shards, in place.  Two barriers
+        order it against every rank's local passes.  Logical exchange count
+        as in the reference (2 per layer)."""
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        global_su2_pass(self._peers, self.k, 1 << self.n_local, self.rank, self.K, [SU2.rx(beta)] * self.k)
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        self.exchange_count += 2
+        instrumentation.bump("exchange", 2)
+
+    def close(self) -> None:
+        for ptr, off in self._opened:
+            _lib.call("fq_ipc_close", ptr, off)
+        self._opened = []
+        self._peers = None
 
     # ------------------------------------------------------------------ XY mixers
     def _xy_gate(self, psi: torch.Tensor, beta: float, i: int, j: int) -> torch.Tensor:

@@ -118,3 +118,19 @@ def test_single_worker_equals_single_node():
     params = QaoaParams(tuple(rng.uniform(-1, 1, 2)), tuple(rng.uniform(-1, 1, 2)))
     np.testing.assert_allclose(D.simulate_qaoa_distributed(poly, params, 1).statevector(),
                                simulate_qaoa(poly, params).state, atol=1e-13)
+
+
+@pytest.mark.parametrize("n,K,p", [(10, 2, 2), (14, 4, 3), (17, 8, 2), (20, 16, 1)])
+def test_fused_global_pass_equals_exchange_path(n, K, p):
+    """The peer-memory global-qubit pass (fq_global_su2_pass) replaces Alg. 4's
+    exchange -> k-position pass -> exchange with identical results and the same
+    logical exchange count."""
+    from paper_2309_04841_b200.distributed import simulate_qaoa_distributed
+
+    rng = np.random.default_rng(n + K)
+    g, b = rng.uniform(0, 1, p), rng.uniform(-1.5, 1.5, p)
+    params = QaoaParams(tuple(g), tuple(b))
+    a = simulate_qaoa_distributed(labs_terms(n), params, K, fused=True)
+    r = simulate_qaoa_distributed(labs_terms(n), params, K, fused=False)
+    np.testing.assert_allclose(a.statevector(), r.statevector(), rtol=0, atol=1e-12)
+    assert a.exchange_count == r.exchange_count == 2 * p

@@ -23,7 +23,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, p, kind, chunk, q):
+def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -35,16 +35,21 @@ def _worker(rank, world, port, n, p, kind, chunk, q):
         rng = np.random.default_rng(11)
         g, b = rng.uniform(0, 1, p), rng.uniform(0, 1, p)
         poly = labs_terms(n) if kind == "x" else portfolio_terms(n)
-        sim = ShardedQaoaSimulator(poly, mixer=kind, chunk_bytes=chunk)
+        sim = ShardedQaoaSimulator(poly, mixer=kind, chunk_bytes=chunk, global_mode=mode)
         E = sim.simulate_qaoa(g, b, initial_weight=None if kind == "x" else n // 2)
         ov = sim.overlap()
         q.put((rank, E, ov, sim.exchange_count, sim.shard.cpu().numpy()))
+        if mode == "p2p":
+            dist.barrier()
+            sim.close()
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,p,kind,chunk", [(16, 3, "x", None), (17, 2, "x", 1 << 16), (14, 2, "xy-ring", None)])
-def test_two_process_sharded_matches_single_gpu(n, p, kind, chunk):
+@pytest.mark.parametrize("n,p,kind,chunk,mode", [(16, 3, "x", None, "exchange"), (17, 2, "x", 1 << 16, "exchange"),
+                                                 (14, 2, "xy-ring", None, "exchange"), (16, 3, "x", None, "p2p"),
+                                                 (19, 2, "x", None, "p2p")])
+def test_two_process_sharded_matches_single_gpu(n, p, kind, chunk, mode):
     from oracle import oracle as O
     from paper_2309_04841_b200 import Mixer, QaoaSimulator, hamming_weight_state
     from paper_2309_04841_b200.problems import labs_terms, portfolio_terms
@@ -53,7 +58,7 @@ def test_two_process_sharded_matches_single_gpu(n, p, kind, chunk):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, p, kind, chunk, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, p, kind, chunk, q, mode)) for r in range(world)]
     for pr in procs:
         pr.start()
     out = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
