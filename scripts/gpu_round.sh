@@ -9,5 +9,6 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_$TAG.log 2>&1; echo "bench exit $?" >> gpurun_out/bench_$TAG.log
 timeout 300 python scripts/bench_pass.py --opts "plan=-1" --detail > gpurun_out/pass_$TAG.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch_$TAG.log 2>&1
+timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:k_pass -s 63 -c 21 --csv --log-file gpurun_out/traffic_$TAG.csv python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_traffic_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pass -s 63 -c 4 -o gpurun_out/prof_$TAG python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_full_$TAG.log 2>&1
 echo done

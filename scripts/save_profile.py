@@ -54,6 +54,21 @@ if os.path.exists(rep):
                              "us": float(d["gpu__time_duration.sum"][0])})
     tr = {"n": 26, "source": f"profiles/{dest}/ncu_full_summary.txt", "launches": launches,
           "dram_bytes_per_launch": sum(x["dram_bytes"] for x in launches) / max(1, len(launches))}
+    tfile = os.path.join(src, f"traffic_{tag}.csv")
+    if os.path.exists(tfile):  # every pass of one step: traffic per launch comparable to bench's algorithmic bytes
+        shutil.copy(tfile, os.path.join(out, "traffic_step.csv"))
+        rows = [r for r in csv.reader(open(tfile)) if len(r) > 10]
+        h = rows[0]
+        ki, mi, ui, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Unit"), h.index("Metric Value")
+        ids = {}
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        for r in rows[1:]:
+            if r[mi].startswith("dram__bytes"):
+                ids.setdefault(r[0], [r[ki], 0.0])[1] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+        if ids:
+            tot = sum(v[1] for v in ids.values())
+            tr.update({"dram_bytes_per_launch": tot / len(ids), "step_launches": len(ids), "step_dram_bytes": tot,
+                       "source": f"profiles/{dest}/traffic_step.csv (all k_pass16 launches of one step)"})
     with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
         json.dump(tr, f, indent=1)
     print(json.dumps(tr, indent=1))
