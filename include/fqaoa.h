@@ -207,8 +207,9 @@ int fq_ipc_open(const void *handle, int64_t offset, void **dev_ptr_out);
 int fq_ipc_close(void *dev_ptr, int64_t offset);
 
 /* HBM passes per layer of the tiled XY program (ring / complete gate order of
- * reference mixers.py:109-125) at n qubits; 1 for n <= 12 (on chip), -1 for other kinds. */
-int fq_plan_xy_passes(int n, int mixer);
+ * reference mixers.py:109-125) at n qubits; 1 for n <= 12 (on chip), -1 for other
+ * kinds.  *rounds (if non-NULL): register rounds summed over the passes. */
+int fq_plan_xy_passes(int n, int mixer, int *rounds);
 
 /* Passes of the last tiled X/custom program run on this host thread's
  * process: returns the pass count; for i < max fills info[5*i..5*i+4] =

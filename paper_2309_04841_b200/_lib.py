@@ -58,7 +58,7 @@ _SIGS = {
     "fq_plan_x_passes": ([I, I, ctypes.POINTER(FqLayer)], I),
     "fq_set_option": ([ctypes.c_char_p, I], I),
     "fq_last_passes": ([P, P, I], I),
-    "fq_plan_xy_passes": ([I, I], I),
+    "fq_plan_xy_passes": ([I, I, P], I),
     "fq_global_su2_pass": ([P, I, I64, I, I, P, P], I),
     "fq_ipc_handle": ([P, P, P], I),
     "fq_ipc_open": ([P, I64, P], I),

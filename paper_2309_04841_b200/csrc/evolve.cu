@@ -635,7 +635,7 @@ static void xy_gates(int n, int kind, std::vector<std::pair<int, int>> &g) {
 
 int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>> &gates, cudaStream_t st,
                  int *passes_out);
-int plan_xy_passes(int n, const std::vector<std::pair<int, int>> &gates);
+int plan_xy_passes(int n, const std::vector<std::pair<int, int>> &gates, int *rounds);
 static int g_xy_tiled = 1;   // tiled XY passes (0: one pair kernel per gate, the reference's structure)
 
 static int run_xy_program(const fq_evolve_desc *d, cudaStream_t st) {
@@ -813,12 +813,13 @@ int fq_plan_x_passes(int n, int n_layers, const fq_layer *layers) {
     return (int)plan_x(n, n_layers, layers, groups, g_fuse != 0).size();
 }
 
-int fq_plan_xy_passes(int n, int mixer) {
+int fq_plan_xy_passes(int n, int mixer, int *rounds) {
+    if (rounds) *rounds = 0;
     if (n <= kTileBits) return 1;
     if (mixer != FQ_MIXER_XY_RING && mixer != FQ_MIXER_XY_COMPLETE) return -1;
     std::vector<std::pair<int, int>> gates;
     xy_gates(n, mixer, gates);
-    return plan_xy_passes(n, gates);
+    return plan_xy_passes(n, gates, rounds);
 }
 
 int fq_last_passes(int *info, float *ms, int max) {

@@ -249,6 +249,63 @@ static std::vector<std::vector<int>> cut_groups(const std::vector<std::pair<int,
     return groups;
 }
 
+// One dependency-respecting scan with a fixed register set R: takes every
+// remaining gate inside R whose qubits no skipped gate has touched.
+static void scan_round(const std::vector<std::pair<int, int>> &gates, const std::vector<int> &idx, const int *R,
+                       std::vector<int> &taken, std::vector<int> &rest) {
+    taken.clear();
+    rest.clear();
+    std::vector<char> blocked(64, 0);
+    auto in_r = [&](int q) { return q == R[0] || q == R[1] || q == R[2] || q == R[3]; };
+    for (int gi : idx) {
+        const int a = gates[gi].first, b = gates[gi].second;
+        if (!blocked[a] && !blocked[b] && in_r(a) && in_r(b)) {
+            taken.push_back(gi);
+        } else {
+            rest.push_back(gi);
+            blocked[a] = blocked[b] = 1;
+        }
+    }
+}
+
+// Register rounds of one pass: each round holds 4 qubits; the first remaining
+// gate's two qubits are always in it and the other two are chosen (exhaustively
+// over the pass's qubits) to maximise the gates the round can take — e.g. a
+// 2 x 2 block (r1, r2) x (c1, c2) of the complete graph's lexicographic order
+// (4 gates) where a plain in-order cut takes 3.
+static std::vector<std::vector<int>> round_cut(const std::vector<std::pair<int, int>> &gates, std::vector<int> idx) {
+    std::vector<std::vector<int>> rounds;
+    std::vector<int> qs;
+    for (int gi : idx)
+        for (int x : {gates[gi].first, gates[gi].second})
+            if (std::find(qs.begin(), qs.end(), x) == qs.end()) qs.push_back(x);
+    std::vector<int> taken, rest, best_taken, best_rest;
+    while (!idx.empty()) {
+        const int a = gates[idx[0]].first, b = gates[idx[0]].second;
+        std::vector<int> others;
+        for (int q : qs)
+            if (q != a && q != b) others.push_back(q);
+        best_taken.clear();
+        if (others.size() < 2) {
+            int R[4] = {a, b, others.empty() ? a : others[0], a};
+            scan_round(gates, idx, R, best_taken, best_rest);
+        } else {
+            for (size_t i = 0; i < others.size(); ++i)
+                for (size_t j = i + 1; j < others.size(); ++j) {
+                    int R[4] = {a, b, others[i], others[j]};
+                    scan_round(gates, idx, R, taken, rest);
+                    if (taken.size() > best_taken.size()) {
+                        best_taken = taken;
+                        best_rest = rest;
+                    }
+                }
+        }
+        rounds.push_back(best_taken);
+        idx = best_rest;
+    }
+    return rounds;
+}
+
 static std::vector<XyPassPlan> plan_xy(int n, const std::vector<std::pair<int, int>> &gates) {
     std::vector<int> all(gates.size());
     for (size_t i = 0; i < gates.size(); ++i) all[i] = (int)i;
@@ -267,7 +324,7 @@ static std::vector<XyPassPlan> plan_xy(int n, const std::vector<std::pair<int, i
         pl.tile = tile_for(n, q);
         auto tbit = [&](int qubit) { return (int)(std::find(pl.tile.begin(), pl.tile.end(), qubit) - pl.tile.begin()); };
         // rounds: 4 register bits
-        for (auto &rg : cut_groups(gates, pg, [](const std::vector<int> &qq) { return qq.size() <= 4; })) {
+        for (auto &rg : round_cut(gates, pg)) {
             std::vector<int> bits;
             std::vector<std::pair<int, int>> gl;
             for (int gi : rg) {
@@ -462,6 +519,13 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
     return FQ_OK;
 }
 
-int plan_xy_passes(int n, const std::vector<std::pair<int, int>> &gates) { return (int)plan_xy(n, gates).size(); }
+int plan_xy_passes(int n, const std::vector<std::pair<int, int>> &gates, int *rounds) {
+    const auto plans = plan_xy(n, gates);
+    if (rounds) {
+        *rounds = 0;
+        for (auto &pl : plans) *rounds += (int)pl.round_bits.size();
+    }
+    return (int)plans.size();
+}
 
 }  // namespace fq
