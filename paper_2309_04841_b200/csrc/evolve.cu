@@ -255,7 +255,8 @@ static int g_prefetch = 1;   // L2 prefetch distance (grid strides)
 static int g_phase_tables = 1;
 static int g_plan = -1;      // -1: choose by cost model, else force candidate
 static int g_time_passes = 0;
-static int g_probe = 0;      // development probe bits (PassParams::probe)  // record a CUDA event after every pass of the next programs
+static int g_probe = 0;      // development probe bits (PassParams::probe)
+static int g_zigzag = 1;     // alternate the tile walk direction pass to pass (L2 reuse across passes)  // record a CUDA event after every pass of the next programs
 
 // Per-pass record of the last X program (fq_last_passes): kind + event timing.
 struct PassRecord {
@@ -586,6 +587,7 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
         P.tile_mask = 0;
         for (int i = 0; i < kTileBits; ++i) P.tile_mask |= 1LL << g.tile_pos[i];
         P.step_dep = deposit(grid, P.tile_mask);
+        P.reverse = g_zigzag ? (int)(si & 1) : 0;
         P.pf_dist = g_prefetch;
         P.probe = g_probe;
         P.run_bits = 0;
@@ -791,6 +793,7 @@ int fq_set_option(const char *name, int value) {
         {"plan", &g_plan, -1, 1},           // group plan: -1 cost model, 0 legacy, 1 small fusion groups
         {"time_passes", &g_time_passes, 0, 1},  // CUDA events around every pass (fq_last_passes)
         {"xy_tiled", &g_xy_tiled, 0, 1},    // tiled XY passes (0: one kernel per gate)
+        {"zigzag", &g_zigzag, 0, 1},        // alternate tile walk direction pass to pass
         {"probe", &g_probe, 0, 7},          // development: isolate phase costs (results invalid when != 0)
     };
     for (auto &o : opts) {

@@ -73,6 +73,7 @@ struct PassParams {
     long long coff[3][kRegs]; // the same in the cost vector (bytes)
     long long tile_mask;      // bits at the tile positions
     long long step_dep;       // pdep(gridDim.x) into the non-tile positions: base(t + grid) = next_base(base(t))
+    int reverse;              // walk the tiles from the top (alternate passes: L2 reuse)
     CoefSet A, B;
 };
 
@@ -264,6 +265,10 @@ __device__ __forceinline__ long long next_base(long long base, long long mask, l
     return ((base | mask) + y) & ~mask;
 }
 
+__device__ __forceinline__ long long prev_base(long long base, long long mask, long long y) {
+    return (base - y) & ~mask;  // borrows pass through the (zero) tile positions
+}
+
 // L2 prefetch of a future tile with ONE instruction: the tile is described
 // by a tensor map (runs of tile bits = full box dims, runs of outer bits =
 // box-1 dims whose coordinates come from the tile number), and
@@ -370,15 +375,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
     if (pf) {  // prologue: tiles 1 .. pf_dist-1 of this CTA
         for (int d = 1; d < P.pf_dist; ++d) {
             const long long tp = blockIdx.x + (long long)d * gridDim.x;
-            if (tp < P.n_tiles) prefetch_tile(P, &tm_state, &tm_cost, tp, !P.init);
+            if (tp < P.n_tiles) prefetch_tile(P, &tm_state, &tm_cost, P.reverse ? P.n_tiles - 1 - tp : tp, !P.init);
         }
     }
     constexpr int CB = COST == FQ_COST_F64 ? 8 : 2;
-    long long base = tile_base(P, blockIdx.x);
-    for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x, base = next_base(base, P.tile_mask, P.step_dep)) {
+    // reverse passes walk the tiles from the top: the previous pass ended there,
+    // so the first tiles read are still in L2 (written moments ago)
+    long long base = tile_base(P, P.reverse ? P.n_tiles - 1 - blockIdx.x : blockIdx.x);
+    for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x,
+                   base = P.reverse ? prev_base(base, P.tile_mask, P.step_dep) : next_base(base, P.tile_mask, P.step_dep)) {
         if (pf) {
             const long long tp = t + (long long)P.pf_dist * gridDim.x;
-            if (tp < P.n_tiles) prefetch_tile(P, &tm_state, &tm_cost, tp, !P.init);
+            if (tp < P.n_tiles) prefetch_tile(P, &tm_state, &tm_cost, P.reverse ? P.n_tiles - 1 - tp : tp, !P.init);
         }
         // per-tile base pointers; the registers' offsets are constant-bank byte offsets
         const char *ps8 = reinterpret_cast<const char *>(P.psi + base + thr8);
