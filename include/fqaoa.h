@@ -88,6 +88,14 @@ int fq_accumulate_terms_dyadic(double *out, int64_t size, const int64_t *iweight
                                const int64_t *masks, int64_t n_terms, int shift, int acc_bits,
                                int64_t index_base, void *stream);
 
+/* The same diagonal (dyadic weights w_t = iweights[t] * 2^-shift, sum |iweights| < 2^53)
+ * as a Walsh-Hadamard transform of the term weights: out = WHT(a), a[m] = sum of the
+ * weights with mask m — n * 2^n exact additions instead of T * 2^n parities, bit-identical
+ * to the reference's sequential sum.  size = 2^n_local >= 4096; a shard's index_base is a
+ * multiple of size (global bits fold into term signs).  Overwrites out. */
+int fq_precompute_wht(double *out, int64_t size, const int64_t *iweights, const int64_t *masks, int64_t n_terms,
+                      int shift, int64_t index_base, void *stream);
+
 /* Same exact-integer accumulation, emitted directly as uint16 levels
  * v = (S(k) - level_offset) >> level_shift where S(k) = sum_t iweights[t]*sign.
  * Used when the float64 diagonal does not fit (n=34, K=2).  *bad_dev (device

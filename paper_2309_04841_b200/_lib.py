@@ -47,6 +47,7 @@ _SIGS = {
     "fq_accumulate_terms": ([P, I64, P, P, I64, I64, P], I),
     "fq_accumulate_terms_dyadic": ([P, I64, P, P, I64, I, I, I64, P], I),
     "fq_precompute_levels_u16": ([P, I64, P, P, I64, I, I64, I64, I, P, P], I),
+    "fq_precompute_wht": ([P, I64, P, P, I64, I, I64, P], I),
     "fq_abs2_inplace": ([P, I64, P], I),
     "fq_init_state": ([P, I64, I, D, I64, P], I),
     "fq_expectation": ([P, P, I, D, D, I64, P, P, P], I),

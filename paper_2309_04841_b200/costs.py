@@ -103,8 +103,21 @@ class DeviceCosts:
             return False
         out = torch.empty(size, dtype=torch.uint16, device=dev)
         bad = torch.zeros(1, dtype=torch.int32, device=dev)
-        _lib.call("fq_precompute_levels_u16", out.data_ptr(), size, iw.data_ptr(), m.data_ptr(),
-                  len(poly.terms), acc_bits, index_base, lo, 0, bad.data_ptr(), _lib.stream())
+        chunk = min(size, 1 << 28)
+        if size >= 4096 and index_base % chunk == 0:
+            # Walsh-Hadamard transform per 2^28-amplitude chunk into a float64 scratch
+            # (2 GiB), then lossless packing: no float64 vector of the whole shard
+            tmp = torch.empty(chunk, dtype=torch.float64, device=dev)
+            scale, offset = 2.0 ** -ta.shift, float(lo) * 2.0 ** -ta.shift
+            for c0 in range(0, size, chunk):
+                _lib.call("fq_precompute_wht", tmp.data_ptr(), chunk, iw.data_ptr(), m.data_ptr(), len(poly.terms),
+                          ta.shift, index_base + c0, _lib.stream())
+                _lib.call("fq_compact_u16", out[c0:c0 + chunk].data_ptr(), tmp.data_ptr(), chunk, scale, offset,
+                          bad.data_ptr(), _lib.stream())
+            del tmp
+        else:
+            _lib.call("fq_precompute_levels_u16", out.data_ptr(), size, iw.data_ptr(), m.data_ptr(),
+                      len(poly.terms), acc_bits, index_base, lo, 0, bad.data_ptr(), _lib.stream())
         if int(bad.item()) != 0:
             return False
         self.u16 = out

@@ -148,3 +148,67 @@ def test_reductions_vs_oracle():
     a = expectation_device(d, dc).item()
     b = expectation_device(d, dc).item()
     assert a == b
+
+
+@pytest.mark.parametrize("case", ["labs", "maxcut_halves", "random_int", "dup_masks"])
+@pytest.mark.parametrize("n", [12, 15, 20, 25])
+def test_wht_diagonal_bit_exact(case, n):
+    """Integer / dyadic diagonals as a Walsh-Hadamard transform of the weights
+    (fq_precompute_wht) equal the reference's per-element sum bit for bit."""
+    import torch
+
+    from paper_2309_04841_b200 import _lib
+    from paper_2309_04841_b200.problems import Graph, labs_terms, maxcut_terms
+    from paper_2309_04841_b200.terms import term_arrays
+
+    rng = np.random.default_rng(n * 7 + len(case))
+    if case == "labs":
+        poly = labs_terms(n)
+    elif case == "maxcut_halves":
+        edges = {tuple(sorted(rng.choice(n, 2, replace=False).tolist())) for _ in range(3 * n)}
+        poly = maxcut_terms(Graph.from_edges(n, sorted(edges)))
+    elif case == "random_int":
+        poly = TermPolynomial.from_pairs(n, random_pairs(rng, n, max_terms=4 * n, integer=True))
+    else:  # repeated supports and a constant: the scatter must add them exactly
+        pairs = [(float(rng.integers(-9, 10)), (1, 3)) for _ in range(5)] + [(2.5, ()), (-0.25, (0, n - 1))] * 3
+        poly = TermPolynomial.from_pairs(n, pairs)
+    pairs = [(t.weight, t.support) for t in poly.terms]
+    ref = O.precompute_cost_vector(n, pairs)
+    ta = term_arrays(poly)
+    assert ta.iweights is not None
+    out = torch.empty(1 << n, dtype=torch.float64, device="cuda")
+    iw, m = torch.from_numpy(ta.iweights).cuda(), torch.from_numpy(ta.masks).cuda()  # alive until the sync below
+    _lib.call("fq_precompute_wht", out.data_ptr(), 1 << n, iw.data_ptr(), m.data_ptr(), len(poly.terms), ta.shift, 0,
+              _lib.stream())
+    np.testing.assert_array_equal(out.cpu().numpy().view(np.uint64), ref.view(np.uint64))
+
+
+def test_wht_diagonal_shards():
+    """A shard [r 2^nl, (r+1) 2^nl) folds the global bits into the term signs."""
+    from paper_2309_04841_b200.problems import labs_terms
+
+    n, nl = 18, 14
+    poly = labs_terms(n)
+    pairs = [(t.weight, t.support) for t in poly.terms]
+    full = O.precompute_cost_vector(n, pairs)
+    for r in range(1 << (n - nl)):
+        got = precompute_device(poly, index_base=r << nl, size=1 << nl).cpu().numpy()
+        np.testing.assert_array_equal(got.view(np.uint64), full[r << nl:(r + 1) << nl].view(np.uint64))
+
+
+def test_u16_levels_via_wht_chunks():
+    """The uint16-only diagonal (capacity path: no float64 vector) built from
+    per-chunk Walsh-Hadamard transforms decodes to the reference diagonal."""
+    from paper_2309_04841_b200.problems import labs_terms
+
+    n = 20
+    poly = labs_terms(n)
+    ref = O.precompute_cost_vector(n, [(t.weight, t.support) for t in poly.terms])
+    dc = DeviceCosts.from_polynomial(poly, keep_f64=False)
+    assert dc.f64 is None
+    lv = dc.u16.cpu().numpy().astype(np.float64)
+    np.testing.assert_array_equal(dc.scale * lv + dc.offset, ref)
+    # a shard of a larger problem (global bits folded into the term signs)
+    dc2 = DeviceCosts.from_polynomial(labs_terms(22), keep_f64=False, index_base=3 << 20, n_local=20)
+    ref2 = O.precompute_cost_vector(22, [(t.weight, t.support) for t in labs_terms(22).terms], base=3 << 20, size=1 << 20)
+    np.testing.assert_array_equal(dc2.scale * dc2.u16.cpu().numpy().astype(np.float64) + dc2.offset, ref2)
