@@ -17,7 +17,7 @@
 #include <cstring>
 #include <vector>
 
-#include "pass.cuh"
+#include "tmap.cuh"
 
 namespace fq {
 
@@ -44,6 +44,9 @@ struct XyParams {
     int tile_pos[kTileBits];
     long long roff_first[kRegs], roff_last[kRegs];  // physical offsets of the registers, first / last round
     int init, expect, table_hi;
+    int pf;                                   // L2 tile prefetch (one tensor-map instruction per tile)
+    int sm_rank, sm_shift[5], sm_bits[5];     // state map
+    int cm_rank, cm_shift[5], cm_bits[5];     // cost map (cm_rank = 0: not needed)
     int nrounds;
     XyRound rounds[kXyMaxRounds];
 };
@@ -125,7 +128,9 @@ __device__ __forceinline__ double2 xy_phase(const XyParams &P, CostRaw<COST> raw
 }
 
 template <int COST, int PH>
-__global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__ XyParams P) {
+__global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__ XyParams P,
+                                                         const __grid_constant__ CUtensorMap tm_state,
+                                                         const __grid_constant__ CUtensorMap tm_cost) {
     extern __shared__ double2 smem[];
     double2 *tile = smem;
     double2 *tlo = smem + kTile;
@@ -141,6 +146,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__
     double eacc = 0.0;
     for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
         const long long base = xy_tile_base(P.tile_pos, t);
+        if (P.pf && tid == 0 && t + gridDim.x < P.n_tiles) {  // next tile of this CTA into L2
+            int c[5];
+            if (!P.init && P.sm_rank) {
+                tile_coords(t + gridDim.x, P.sm_rank, P.sm_shift, P.sm_bits, c);
+                tensor_prefetch_l2(&tm_state, P.sm_rank, c);
+            }
+            if (P.cm_rank) {
+                tile_coords(t + gridDim.x, P.cm_rank, P.cm_shift, P.cm_bits, c);
+                tensor_prefetch_l2(&tm_cost, P.cm_rank, c);
+            }
+        }
         double2 v[kRegs];
         if (P.init) {
 #pragma unroll
@@ -423,8 +439,13 @@ static void fill_round(XyRound &R, const std::vector<int> &bits, const std::vect
     }
 }
 
+struct XyMaps {
+    alignas(64) CUtensorMap state;
+    alignas(64) CUtensorMap cost;
+};
+
 template <int COST, int PH>
-static int launch_xy(const XyParams &P, int grid, cudaStream_t st) {
+static int launch_xy(const XyParams &P, const XyMaps &M, int grid, cudaStream_t st) {
     static bool configured = false;
     const size_t smem = (size_t)(kTile + (kTableLo + kMaxTableHi) * kCopies) * sizeof(double2);
     if (!configured) {
@@ -433,7 +454,7 @@ static int launch_xy(const XyParams &P, int grid, cudaStream_t st) {
     }
     const size_t need = (size_t)(kTile + (PH && COST == FQ_COST_U16 ? (kTableLo + P.table_hi) * kCopies : 0)) *
                         sizeof(double2);
-    k_xy_pass<COST, PH><<<grid, kThreads, need, st>>>(P);
+    k_xy_pass<COST, PH><<<grid, kThreads, need, st>>>(P, M.state, M.cost);
     FQ_LAUNCHED("k_xy_pass");
     return FQ_OK;
 }
@@ -495,9 +516,20 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
                 P->roff_last[i] = b;
             }
             const bool ph = pi == 0 && L.apply_phase && L.gamma != 0.0;
+            XyMaps M;
+            std::memset(&M, 0, sizeof M);
+            P->pf = 1;
+            P->sm_rank = build_tile_map(&M.state, psi, n, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2,
+                                        P->sm_shift, P->sm_bits);
+            if (ph || P->expect)
+                P->cm_rank = d->cost_kind == FQ_COST_F64
+                                 ? build_tile_map(&M.cost, d->costs, n, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
+                                                  1, P->cm_shift, P->cm_bits)
+                                 : build_tile_map(&M.cost, d->costs, n, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
+                                                  1, P->cm_shift, P->cm_bits);
             int s;
-            if (d->cost_kind == FQ_COST_U16) s = ph ? launch_xy<FQ_COST_U16, 1>(*P, grid, st) : launch_xy<FQ_COST_U16, 0>(*P, grid, st);
-            else s = ph ? launch_xy<FQ_COST_F64, 1>(*P, grid, st) : launch_xy<FQ_COST_F64, 0>(*P, grid, st);
+            if (d->cost_kind == FQ_COST_U16) s = ph ? launch_xy<FQ_COST_U16, 1>(*P, M, grid, st) : launch_xy<FQ_COST_U16, 0>(*P, M, grid, st);
+            else s = ph ? launch_xy<FQ_COST_F64, 1>(*P, M, grid, st) : launch_xy<FQ_COST_F64, 0>(*P, M, grid, st);
             if (s) {
                 delete P;
                 return s;
