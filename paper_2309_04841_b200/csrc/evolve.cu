@@ -524,13 +524,13 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
         PassMaps M;
         std::memset(&M, 0, sizeof M);
         if (P.pf_dist > 0) {
-            P.sm_rank = build_tile_map(&M.state, psi, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2, P.sm_shift,
+            P.sm_rank = cached_tile_map(&M.state, psi, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2, P.sm_shift,
                                        P.sm_bits);
             if (P.pf_cost)
                 P.cm_rank = d->cost_kind == FQ_COST_F64
-                                ? build_tile_map(&M.cost, d->costs, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 1,
+                                ? cached_tile_map(&M.cost, d->costs, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 1,
                                                  P.cm_shift, P.cm_bits)
-                                : build_tile_map(&M.cost, d->costs, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, 1,
+                                : cached_tile_map(&M.cost, d->costs, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, 1,
                                                  P.cm_shift, P.cm_bits);
             if (P.sm_rank == 0 && P.cm_rank == 0) P.pf_dist = 0;
         }

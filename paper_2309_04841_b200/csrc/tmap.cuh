@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "pass.cuh"
@@ -79,6 +80,49 @@ static inline int build_tile_map(CUtensorMap *map, const void *gaddr, int n, con
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? rank : 0;
+}
+
+// Encoding a map costs a few microseconds of host time per pass; a program
+// re-encodes the same (buffer, tile) pairs every call (the caching allocator
+// hands back the same state buffer), so maps are memoised.
+struct TileMapKey {
+    const void *addr;
+    int n, dt, elem_bytes, per_amp;
+    long long tile_mask;
+    bool operator==(const TileMapKey &o) const {
+        return addr == o.addr && n == o.n && dt == o.dt && elem_bytes == o.elem_bytes && per_amp == o.per_amp &&
+               tile_mask == o.tile_mask;
+    }
+};
+struct TileMapEntry {
+    TileMapKey key;
+    alignas(64) CUtensorMap map;
+    int rank, shift[5], bits[5];
+};
+
+static inline int cached_tile_map(CUtensorMap *map, const void *gaddr, int n, const int *tile_pos,
+                                  CUtensorMapDataType dt, int elem_bytes, int per_amp, int *outer_shift,
+                                  int *outer_bits) {
+    static std::vector<TileMapEntry> cache;  // small: a few groups x (state, costs)
+    static size_t next = 0;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    TileMapKey key{gaddr, n, (int)dt, elem_bytes, per_amp, 0};
+    for (int i = 0; i < 12; ++i) key.tile_mask |= 1LL << tile_pos[i];
+    for (auto &e : cache)
+        if (e.key == key) {
+            *map = e.map;
+            for (int d = 0; d < 5; ++d) outer_shift[d] = e.shift[d], outer_bits[d] = e.bits[d];
+            return e.rank;
+        }
+    TileMapEntry e;
+    e.key = key;
+    e.rank = build_tile_map(&e.map, gaddr, n, tile_pos, dt, elem_bytes, per_amp, e.shift, e.bits);
+    if (cache.size() < 64) cache.push_back(e);
+    else cache[next++ % 64] = e;
+    *map = e.map;
+    for (int d = 0; d < 5; ++d) outer_shift[d] = e.shift[d], outer_bits[d] = e.bits[d];
+    return e.rank;
 }
 
 }  // namespace fq

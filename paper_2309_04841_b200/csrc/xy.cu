@@ -519,13 +519,13 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
             XyMaps M;
             std::memset(&M, 0, sizeof M);
             P->pf = 1;
-            P->sm_rank = build_tile_map(&M.state, psi, n, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2,
+            P->sm_rank = cached_tile_map(&M.state, psi, n, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2,
                                         P->sm_shift, P->sm_bits);
             if (ph || P->expect)
                 P->cm_rank = d->cost_kind == FQ_COST_F64
-                                 ? build_tile_map(&M.cost, d->costs, n, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
+                                 ? cached_tile_map(&M.cost, d->costs, n, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
                                                   1, P->cm_shift, P->cm_bits)
-                                 : build_tile_map(&M.cost, d->costs, n, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
+                                 : cached_tile_map(&M.cost, d->costs, n, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
                                                   1, P->cm_shift, P->cm_bits);
             int s;
             if (d->cost_kind == FQ_COST_U16) s = ph ? launch_xy<FQ_COST_U16, 1>(*P, M, grid, st) : launch_xy<FQ_COST_U16, 0>(*P, M, grid, st);
