@@ -565,8 +565,9 @@ static void xy_gates(int n, int kind, std::vector<std::pair<int, int>> &g) {
 
 int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>> &gates, cudaStream_t st,
                  int *passes_out);
-int plan_xy_passes(int n, const std::vector<std::pair<int, int>> &gates, int *rounds);
+int plan_xy_passes(int n, int mixer, const std::vector<std::pair<int, int>> &gates, int *rounds);
 static int g_xy_tiled = 1;   // tiled XY passes (0: one pair kernel per gate, the reference's structure)
+extern int g_xy_min_run;     // xy.cu
 
 static int run_xy_program(const fq_evolve_desc *d, cudaStream_t st) {
     const int n = d->n;
@@ -722,6 +723,7 @@ int fq_set_option(const char *name, int value) {
         {"time_passes", &g_time_passes, 0, 1},  // CUDA events around every pass (fq_last_passes)
         {"xy_tiled", &g_xy_tiled, 0, 1},    // tiled XY passes (0: one kernel per gate)
         {"zigzag", &g_zigzag, 0, 1},        // alternate tile walk direction pass to pass
+        {"xy_min_run", &g_xy_min_run, 0, 8},  // XY pass tiles: min contiguous run, log2 amplitudes (0 = auto)
         {"probe", &g_probe, 0, 7},          // development: isolate phase costs (results invalid when != 0)
     };
     for (auto &o : opts) {
@@ -750,7 +752,7 @@ int fq_plan_xy_passes(int n, int mixer, int *rounds) {
     if (mixer != FQ_MIXER_XY_RING && mixer != FQ_MIXER_XY_COMPLETE) return -1;
     std::vector<std::pair<int, int>> gates;
     xy_gates(n, mixer, gates);
-    return plan_xy_passes(n, gates, rounds);
+    return plan_xy_passes(n, mixer, gates, rounds);
 }
 
 int fq_last_passes(int *info, float *ms, int max) {

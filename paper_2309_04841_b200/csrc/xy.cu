@@ -22,6 +22,7 @@
 namespace fq {
 
 constexpr int kXyMaxRounds = 24;
+int g_xy_min_run = 0;  // minimum contiguous run (log2 amplitudes) of an XY pass tile; 0 = per mixer (measured)
 constexpr int kXyMaxGates = 6;  // C(4, 2): distinct pairs of one 4-bit register set
 
 struct XyRound {
@@ -322,12 +323,19 @@ static std::vector<std::vector<int>> round_cut(const std::vector<std::pair<int, 
     return rounds;
 }
 
-static std::vector<XyPassPlan> plan_xy(int n, const std::vector<std::pair<int, int>> &gates) {
+// B200, portfolio n = 26: 64-B runs are the best trade for the ring's few
+// passes, 512-B runs for the complete graph's many (scripts/bench_configs.py, FQ_OPTS)
+static int xy_min_run(int mixer) {
+    if (g_xy_min_run > 0) return g_xy_min_run;
+    return mixer == FQ_MIXER_XY_RING ? 3 : 5;
+}
+
+static std::vector<XyPassPlan> plan_xy(int n, const std::vector<std::pair<int, int>> &gates, int min_run) {
     std::vector<int> all(gates.size());
     for (size_t i = 0; i < gates.size(); ++i) all[i] = (int)i;
     // passes: the tile (targets + spectators) must keep runs of >= 16 amplitudes
     auto pass_fits = [&](const std::vector<int> &q) {
-        return (int)q.size() <= kTileBits && run_bits_of(tile_for(n, q)) >= 4;
+        return (int)q.size() <= kTileBits && run_bits_of(tile_for(n, q)) >= min_run;
     };
     std::vector<XyPassPlan> plans;
     for (auto &pg : cut_groups(gates, all, pass_fits)) {
@@ -465,7 +473,7 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
     const int n = d->n;
     const long long size = 1LL << n;
     double2 *psi = static_cast<double2 *>(d->psi);
-    const auto plans = plan_xy(n, gates);
+    const auto plans = plan_xy(n, gates, xy_min_run(d->mixer));
     for (auto &pl : plans)
         if ((int)pl.round_bits.size() > kXyMaxRounds) {
             set_error("run_xy_tiled: a pass needs %d register rounds (max %d)", (int)pl.round_bits.size(),
@@ -551,8 +559,8 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
     return FQ_OK;
 }
 
-int plan_xy_passes(int n, const std::vector<std::pair<int, int>> &gates, int *rounds) {
-    const auto plans = plan_xy(n, gates);
+int plan_xy_passes(int n, int mixer, const std::vector<std::pair<int, int>> &gates, int *rounds) {
+    const auto plans = plan_xy(n, gates, xy_min_run(mixer));
     if (rounds) {
         *rounds = 0;
         for (auto &pl : plans) *rounds += (int)pl.round_bits.size();

@@ -227,6 +227,11 @@ def main():
             subprocess.run(cmd + (["--skip-cpu"] if args.skip_cpu else []), check=False)
         return
     torch.cuda.set_device(0)
+    from paper_2309_04841_b200 import _lib
+
+    for kv in filter(None, os.environ.get("FQ_OPTS", "").split(",")):  # e.g. FQ_OPTS=xy_min_run=5
+        k, v = kv.split("=")
+        _lib.call("fq_set_option", k.encode(), int(v))
     fns = {"1": config1, "2": config2, "3": config3, "4": config4, "5": config5}
     try:
         fns[only[0]](args)
