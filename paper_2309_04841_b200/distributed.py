@@ -306,6 +306,17 @@ def simulate_qaoa_distributed(problem, params: QaoaParams, K: int, mixer: "str |
     sc = ShardedCosts(n, k, _slice_device_costs(dc, K))
     n_local = n - k
     for gamma, beta in zip(params.gammas, params.betas):
+        if mixer.kind == "custom" and k > 0 and fused and k <= 4:
+            us = list(mixer.su2_factory(beta))
+            if len(us) != n:
+                raise ValueError(f"expected {n} matrices, got {len(us)}")
+            table = su2_table([us[:n_local]])
+            for shard, c in zip(sharded.shards, sc.shards):
+                run_program(shard, n_local, "custom", [(gamma, beta, 1, 0, n_local)], dc=c, su2=table)
+            global_su2_pass([s.data_ptr() for s in sharded.shards], k, 1 << n_local, 0, 1, us[n_local:])
+            sharded.exchange_count += 2
+            instrumentation.bump("exchange", 2)
+            continue
         if mixer.kind == "x" and k > 0:
             for shard, c in zip(sharded.shards, sc.shards):
                 run_program(shard, n_local, "x", [(gamma, beta, 1, 0, n_local)], dc=c)
@@ -416,8 +427,6 @@ class ShardedQaoaSimulator:
         params = QaoaParams(tuple(gammas), tuple(betas))
         if self.mixer.preserves_hamming_weight and initial_weight is None:
             raise ValueError("XY mixers need initial_weight (Hamming-weight sector)")
-        if self.mixer.kind == "custom":
-            raise NotImplementedError("multi-process sharding supports the X and XY mixers")
         if self.mixer.preserves_hamming_weight:
             return self._simulate_xy(params, initial_weight, expectation)
         nl, k = self.n_local, self.k
@@ -429,13 +438,25 @@ class ShardedQaoaSimulator:
             psi = self.ops.empty(nl) if initial_weight is None else self.initial_state(initial_weight)
         init = initial_weight is None
         amp = 1.0 / sqrt(float(2 ** self.n)) if init else 0.0
+        custom = self.mixer.kind == "custom"
         for li, (g, b) in enumerate(zip(params.gammas, params.betas)):
-            self.ops.program(psi, nl, "x", [(g, b, 1, 0, nl)], self.costs, init=init and li == 0, init_amp=amp)
+            us = None
+            if custom:
+                us = list(self.mixer.su2_factory(b))
+                if len(us) != self.n:
+                    raise ValueError(f"expected {self.n} matrices, got {len(us)}")
+            self.ops.program(psi, nl, self.mixer.kind, [(g, b, 1, 0, nl)], self.costs, init=init and li == 0,
+                             init_amp=amp, su2=su2_table([us[:nl]]) if custom else None)
+            glob = us[nl:] if custom else [SU2.rx(b)] * k
             if k > 0 and self.global_mode == "p2p":
-                self._global_p2p(b)
+                self._global_p2p(glob)
             elif k > 0:
                 psi = self.exchange(psi)
-                self.ops.program(psi, nl, "x", [(0.0, b, 0, nl - k, nl)], None)
+                if custom:  # former global qubit n-k+j sits at local position nl-k+j (Alg. 4)
+                    table = [SU2.identity()] * (nl - k) + glob
+                    self.ops.program(psi, nl, "custom", [(0.0, b, 0, nl - k, nl)], None, su2=su2_table([table]))
+                else:
+                    self.ops.program(psi, nl, "x", [(0.0, b, 0, nl - k, nl)], None)
                 psi = self.exchange(psi)
         if params.p == 0 and init:
             psi = self.ops.uniform(self.n, nl)
@@ -471,7 +492,7 @@ class ShardedQaoaSimulator:
             self._peers = peers
         return self._p2p_buf
 
-    def _global_p2p(self, beta: float) -> None:
+    def _global_p2p(self, us: Sequence[SU2]) -> None:
         """Alg. 4's exchange -> k-position pass -> exchange as ONE peer-memory
         kernel per rank (fq_global_su2_pass): rank r transforms the local
         indices of its 1/K part across all K shards, in place.  Two barriers
@@ -479,7 +500,7 @@ class ShardedQaoaSimulator:
         as in the reference (2 per layer)."""
         torch.cuda.synchronize()
         dist.barrier(group=self.group)
-        global_su2_pass(self._peers, self.k, 1 << self.n_local, self.rank, self.K, [SU2.rx(beta)] * self.k)
+        global_su2_pass(self._peers, self.k, 1 << self.n_local, self.rank, self.K, us)
         torch.cuda.synchronize()
         dist.barrier(group=self.group)
         self.exchange_count += 2
@@ -579,8 +600,8 @@ class CudaLocalOps:
                   _lib.stream())
         return psi
 
-    def program(self, psi, n_local, kind, layers, costs, init=False, init_amp=0.0):
-        run_program(psi, n_local, kind, layers, dc=costs, init=init, init_amp=init_amp)
+    def program(self, psi, n_local, kind, layers, costs, init=False, init_amp=0.0, su2=None):
+        run_program(psi, n_local, kind, layers, dc=costs, su2=su2, init=init, init_amp=init_amp)
 
     def xy(self, psi, beta, lo, hi):
         _lib.call("fq_xy_on_pairs", psi.data_ptr(), psi.numel(), float(np.cos(beta)), float(np.sin(beta)), lo, hi,

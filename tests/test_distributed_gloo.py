@@ -42,16 +42,20 @@ class OracleOps:
         pop = np.array([bin(int(i)).count("1") for i in idx])
         return torch.from_numpy(np.where(pop == weight, 1.0 / sqrt(comb(n, weight)), 0.0).astype(np.complex128))
 
-    def program(self, psi, n_local, kind, layers, costs, init=False, init_amp=0.0):
-        assert kind == "x"
+    def program(self, psi, n_local, kind, layers, costs, init=False, init_amp=0.0, su2=None):
+        assert kind in ("x", "custom")
         st = psi.numpy()
         if init:
             st[:] = init_amp
-        for g, b, ph, lo, hi in layers:
+        for li, (g, b, ph, lo, hi) in enumerate(layers):
             if ph and g != 0.0:
                 O.apply_phase(st, costs, g)
-            a, bb = O.rx_coeffs(b)
             for q in range(lo, hi):
+                if kind == "x":
+                    a, bb = O.rx_coeffs(b)
+                else:
+                    c = su2[li][q]
+                    a, bb = complex(c[0], c[1]), complex(c[2], c[3])
                 O.su2_on_pairs(st, a, bb, q)
 
     def xy(self, psi, beta, lo, hi):
@@ -172,3 +176,51 @@ def test_sharded_xy_world2_matches_single_node(kind):
     for rank, E, ex, state in out:
         assert E == pytest.approx(O.expectation(ref, costs), rel=1e-12, abs=1e-12)
     np.testing.assert_allclose(out[0][3], ref, rtol=0, atol=1e-12)
+
+
+def _custom_worker(rank, world, port, n, p, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2309_04841_b200.distributed import ShardedQaoaSimulator
+        from paper_2309_04841_b200.mixers import SU2, Mixer
+        from paper_2309_04841_b200.problems import labs_terms
+
+        rng = np.random.default_rng(3)
+        g, b = rng.uniform(0, 1, p), rng.uniform(0, 1, p)
+        mixer = Mixer.custom(lambda beta: [SU2(np.cos(beta + 0.1 * j), np.sin(beta + 0.1 * j)) for j in range(n)])
+        sim = ShardedQaoaSimulator(labs_terms(n), mixer=mixer, local_ops=OracleOps())
+        E = sim.simulate_qaoa(g, b)
+        shards = [torch.empty_like(sim.shard) for _ in range(world)]
+        dist.all_gather(shards, sim.shard)
+        q.put((rank, E, sim.exchange_count, torch.cat(shards).numpy() if rank == 0 else None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_custom_mixer_world2():
+    """Custom per-qubit SU(2) mixers over 2 ranks (Alg. 4 with arbitrary gates:
+    distributed.py:137-153)."""
+    n, p, world = 9, 2, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_custom_worker, args=(r, world, port, n, p, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    rng = np.random.default_rng(3)
+    g, b = rng.uniform(0, 1, p), rng.uniform(0, 1, p)
+    costs = O.precompute_cost_vector(n, O.labs_terms(n))
+    factory = lambda beta: [(complex(np.cos(beta + 0.1 * j)), complex(np.sin(beta + 0.1 * j))) for j in range(n)]
+    st = O.uniform_state(n)
+    for gg, bb in zip(g, b):
+        O.apply_phase(st, costs, gg)
+        for qb, (a, bc) in enumerate(factory(bb)):
+            O.su2_on_pairs(st, a, bc, qb)
+    np.testing.assert_allclose(out[0][3], st, rtol=0, atol=1e-12)
+    assert out[0][2] == 2 * p

@@ -134,3 +134,25 @@ def test_fused_global_pass_equals_exchange_path(n, K, p):
     r = simulate_qaoa_distributed(labs_terms(n), params, K, fused=False)
     np.testing.assert_allclose(a.statevector(), r.statevector(), rtol=0, atol=1e-12)
     assert a.exchange_count == r.exchange_count == 2 * p
+
+
+@pytest.mark.parametrize("n,K", [(9, 2), (12, 4), (15, 8)])
+def test_fused_global_pass_custom_mixer(n, K):
+    """Custom per-qubit SU(2) mixers: peer-memory global pass == exchange path."""
+    from paper_2309_04841_b200 import Mixer
+    from paper_2309_04841_b200.distributed import simulate_qaoa_distributed
+
+    rng = np.random.default_rng(n)
+    tabs = {}
+
+    def factory(beta):
+        if beta not in tabs:
+            tabs[beta] = [SU2(*random_su2_coeffs(rng)) for _ in range(n)]
+        return tabs[beta]
+
+    params = QaoaParams(tuple(rng.uniform(0, 1, 2)), (0.3, 0.7))
+    mixer = Mixer.custom(factory)
+    a = simulate_qaoa_distributed(labs_terms(n), params, K, mixer=mixer, fused=True)
+    r = simulate_qaoa_distributed(labs_terms(n), params, K, mixer=mixer, fused=False)
+    np.testing.assert_allclose(a.statevector(), r.statevector(), rtol=0, atol=1e-12)
+    assert a.exchange_count == r.exchange_count == 4

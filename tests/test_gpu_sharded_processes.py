@@ -23,6 +23,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def _mixer(kind, n):
+    from paper_2309_04841_b200.mixers import SU2, Mixer
+
+    if kind != "custom":
+        return Mixer(kind)
+    return Mixer.custom(lambda beta: [SU2(np.cos(beta * (1 + 0.05 * j)), -1j * np.sin(beta * (1 + 0.05 * j)))
+                                      for j in range(n)])
+
+
 def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -34,9 +43,9 @@ def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange"):
 
         rng = np.random.default_rng(11)
         g, b = rng.uniform(0, 1, p), rng.uniform(0, 1, p)
-        poly = labs_terms(n) if kind == "x" else portfolio_terms(n)
-        sim = ShardedQaoaSimulator(poly, mixer=kind, chunk_bytes=chunk, global_mode=mode)
-        E = sim.simulate_qaoa(g, b, initial_weight=None if kind == "x" else n // 2)
+        poly = labs_terms(n) if kind in ("x", "custom") else portfolio_terms(n)
+        sim = ShardedQaoaSimulator(poly, mixer=_mixer(kind, n), chunk_bytes=chunk, global_mode=mode)
+        E = sim.simulate_qaoa(g, b, initial_weight=n // 2 if kind.startswith("xy") else None)
         ov = sim.overlap()
         q.put((rank, E, ov, sim.exchange_count, sim.shard.cpu().numpy()))
         if mode == "p2p":
@@ -48,7 +57,8 @@ def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange"):
 
 @pytest.mark.parametrize("n,p,kind,chunk,mode", [(16, 3, "x", None, "exchange"), (17, 2, "x", 1 << 16, "exchange"),
                                                  (14, 2, "xy-ring", None, "exchange"), (16, 3, "x", None, "p2p"),
-                                                 (19, 2, "x", None, "p2p")])
+                                                 (19, 2, "x", None, "p2p"), (15, 2, "custom", None, "p2p"),
+                                                 (15, 2, "custom", None, "exchange")])
 def test_two_process_sharded_matches_single_gpu(n, p, kind, chunk, mode):
     from oracle import oracle as O
     from paper_2309_04841_b200 import Mixer, QaoaSimulator, hamming_weight_state
@@ -67,14 +77,14 @@ def test_two_process_sharded_matches_single_gpu(n, p, kind, chunk, mode):
         assert pr.exitcode == 0
     rng = np.random.default_rng(11)
     g, b = rng.uniform(0, 1, p), rng.uniform(0, 1, p)
-    poly = labs_terms(n) if kind == "x" else portfolio_terms(n)
-    sim = QaoaSimulator(terms=poly, mixer=Mixer(kind))
-    init = None if kind == "x" else hamming_weight_state(n, n // 2)
+    poly = labs_terms(n) if kind in ("x", "custom") else portfolio_terms(n)
+    sim = QaoaSimulator(terms=poly, mixer=_mixer(kind, n))
+    init = hamming_weight_state(n, n // 2) if kind.startswith("xy") else None
     res = sim.simulate_qaoa(g, b, initial=init)
     full = np.concatenate([o[4] for o in out])
     np.testing.assert_allclose(full, res.state, rtol=0, atol=1e-12)
     for rank, E, ov, ex, _ in out:
         assert E == pytest.approx(sim.get_expectation(res), rel=1e-10, abs=1e-12)
         assert ov == pytest.approx(sim.get_overlap(res), abs=1e-12)
-        if kind == "x":
-            assert ex == 2 * p  # Alg. 4: two exchanges per X layer
+        if kind in ("x", "custom"):
+            assert ex == 2 * p  # Alg. 4: two exchanges per layer
