@@ -14,6 +14,15 @@ hypothesis.settings.load_profile("default")
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
+    # the native libraries are build artefacts (git-ignored): build them if missing or stale
+    # (nvcc cross-compiles sm_100a without a GPU; the oracle is plain gcc)
+    from paper_2309_04841_b200 import _build
+
+    if _build._stale():
+        _build.build()
+    from oracle import oracle as O
+
+    O.build()
 
 
 @pytest.fixture(scope="session")
