@@ -184,7 +184,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=0, help="total qubits (default 26 + log2 N)")
+    ap.add_argument("--qubits", "--n", dest="n", type=int, default=0, help="total qubits (default 26 + log2 N)")
     ap.add_argument("--p", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--global-mode", default="p2p", choices=["p2p", "exchange"],
@@ -203,9 +203,17 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # FQ_BENCH_ONE_DEVICE=1: validation of the multi-process path on a one-GPU box
+    # (every rank on cuda:0, gloo for the host-side collectives; timings not meaningful)
+    one_device = os.environ.get("FQ_BENCH_ONE_DEVICE") == "1"
+    if one_device:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2309_04841_b200 import QaoaSimulator, _lib, labs_terms
     from paper_2309_04841_b200.distributed import ShardedQaoaSimulator
     from paper_2309_04841_b200.mixers import run_program
@@ -388,8 +396,10 @@ def main():
                          f"oracle C/OpenMP port, extrapolated to the p={p} evaluation "
                          f"({1e3 * t_layer:.0f} ms/layer, {1e3 * t_exp:.0f} ms expectation)"}
 
+    objective = float(exp_dev.item()) if world == 1 else float(sim.expectation())  # collective for N > 1
     if rank == 0:
         line = {
+            **({"validation_only": "all ranks on one GPU (FQ_BENCH_ONE_DEVICE)"} if one_device else {}),
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128", "data": "synthetic",
@@ -418,7 +428,7 @@ def main():
             "clocks": sampler.summary(),
             "precompute_s": precompute_s,
             "ms_per_layer": ms_step / p,
-            "objective": float(exp_dev.item()) if world == 1 else None,
+            "objective": objective,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
