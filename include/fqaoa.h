@@ -214,6 +214,14 @@ int fq_ipc_handle(const void *dev_ptr, void *handle_out, int64_t *offset_out);
 int fq_ipc_open(const void *handle, int64_t offset, void **dev_ptr_out);
 int fq_ipc_close(void *dev_ptr, int64_t offset);
 
+/* Stream-ordered barrier over peer memory (no host synchronisation):
+ * flag_arrays[q] = rank q's uint32[K] flag array (peer-mapped, zero-initialised);
+ * rank `rank` stores `epoch` into slot `rank` of every array, then waits until
+ * all K slots of its own array reach `epoch` (epochs increase by one per
+ * barrier, identically on every rank).  On a ~10 s timeout *err_dev is set and
+ * the kernel returns.  K <= 16. */
+int fq_peer_barrier(void *const *flag_arrays, int K, int rank, unsigned epoch, int *err_dev, void *stream);
+
 /* HBM passes per layer of the tiled XY program (ring / complete gate order of
  * reference mixers.py:109-125) at n qubits; 1 for n <= 12 (on chip), -1 for other
  * kinds.  *rounds (if non-NULL): register rounds summed over the passes. */

@@ -64,6 +64,7 @@ _SIGS = {
     "fq_ipc_handle": ([P, P, P], I),
     "fq_ipc_open": ([P, I64, P], I),
     "fq_ipc_close": ([P, I64], I),
+    "fq_peer_barrier": ([P, I, I, ctypes.c_uint, P, P], I),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -57,6 +57,45 @@ __global__ void __launch_bounds__(256) k_global_su2(const __grid_constant__ Glob
     }
 }
 
+// Device-side barrier over peer memory: rank r stores `epoch` into slot r of
+// every rank's flag array (remote stores over NVLink), then spins until all K
+// slots of its own array reach `epoch`.  Stream-ordered: the work enqueued
+// before it on every rank is complete (and, after the system fence, visible
+// to the peers) when any rank passes it — no host synchronisation.  A rank
+// that never arrives trips the timeout (~10 s of clock64): *err is set and the
+// kernel returns instead of hanging the device.
+struct BarrierParams {
+    unsigned *flags[1 << kMaxGlobal];  // rank q's flag array (K slots), peer-mapped
+    int K, rank;
+    unsigned epoch;
+    int *err;
+    long long timeout;  // clock64 cycles
+};
+
+__global__ void k_peer_barrier(const __grid_constant__ BarrierParams P) {
+    const int t = threadIdx.x;
+    __threadfence_system();
+    __syncthreads();
+    if (t < P.K) {
+        volatile unsigned *remote = P.flags[t];
+        remote[P.rank] = P.epoch;
+    }
+    __threadfence_system();
+    if (t < P.K) {
+        volatile unsigned *mine = P.flags[P.rank];
+        const long long t0 = clock64();
+        while ((int)(mine[t] - P.epoch) < 0) {
+            if (clock64() - t0 > P.timeout) {
+                atomicExch(P.err, 1);
+                break;
+            }
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+    __threadfence_system();
+}
+
 }  // namespace fq
 
 using namespace fq;
@@ -129,6 +168,23 @@ int fq_ipc_open(const void *handle, int64_t offset, void **dev_ptr_out) {
     void *base = nullptr;
     FQ_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
     *dev_ptr_out = static_cast<char *>(base) + offset;
+    return FQ_OK;
+}
+
+int fq_peer_barrier(void *const *flag_arrays, int K, int rank, unsigned epoch, int *err_dev, void *stream) {
+    FQ_CHECK_ARG(flag_arrays && err_dev && K >= 1 && K <= (1 << kMaxGlobal) && rank >= 0 && rank < K,
+                 "fq_peer_barrier: bad arguments (K <= %d)", 1 << kMaxGlobal);
+    BarrierParams P;
+    for (int q = 0; q < K; ++q) P.flags[q] = static_cast<unsigned *>(flag_arrays[q]);
+    P.K = K;
+    P.rank = rank;
+    P.epoch = epoch;
+    P.err = err_dev;
+    int rate = 0;
+    cudaDeviceGetAttribute(&rate, cudaDevAttrClockRate, 0);  // kHz
+    P.timeout = (long long)(rate > 0 ? rate : 2000000) * 1000LL * 10;  // ~10 s
+    k_peer_barrier<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(P);
+    FQ_LAUNCHED("k_peer_barrier");
     return FQ_OK;
 }
 

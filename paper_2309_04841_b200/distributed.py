@@ -350,7 +350,7 @@ class ShardedQaoaSimulator:
 
     def __init__(self, poly: TermPolynomial, group=None, mixer: "str | Mixer" = "x",
                  compact: bool = True, keep_f64: bool | None = None, chunk_bytes: int | None = None,
-                 local_ops=None, global_mode: str = "exchange"):
+                 local_ops=None, global_mode: str = "exchange", device_barrier: bool = True):
         self.group = group
         self.K = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -371,9 +371,12 @@ class ShardedQaoaSimulator:
         if global_mode not in ("exchange", "p2p"):
             raise ValueError(f"global_mode must be 'exchange' or 'p2p', got {global_mode!r}")
         self.global_mode = global_mode
+        self.device_barrier = device_barrier
         self._p2p_buf = None
         self._peers: list[int] | None = None
+        self._flag_ptrs: list[int] | None = None
         self._opened: list[tuple[int, int]] = []
+        self._epoch = 0
 
     # ------------------------------------------------------------------ exchange
     def exchange(self, shard: torch.Tensor) -> torch.Tensor:
@@ -471,26 +474,52 @@ class ShardedQaoaSimulator:
         all-gathered once).  NVLink peers on one node; on one device (tests)
         the same IPC path maps another process's allocation."""
         if self._p2p_buf is None:
+            self._p2p_buf = self.ops.empty(self.n_local)
+            # flag arrays of the device-side barrier (K uint32 slots per rank) + error word
+            self._flags = torch.zeros(self.K + 1, dtype=torch.int32, device=self._p2p_buf.device)
+            torch.cuda.synchronize()  # zeroed before any peer can store into it
+            self._peers = self._map_peers(self._p2p_buf.data_ptr())
+            self._flag_ptrs = self._map_peers(self._flags.data_ptr())
+        return self._p2p_buf
+
+    def _map_peers(self, ptr: int) -> list[int]:
+        """All-gather the CUDA IPC handle of a local buffer; map every peer's."""
+        import ctypes
+
+        h = (ctypes.c_char * 64)()
+        off = ctypes.c_int64()
+        _lib.call("fq_ipc_handle", ptr, h, ctypes.byref(off))
+        allh = [None] * self.K
+        dist.all_gather_object(allh, (bytes(h), off.value), group=self.group)
+        out = []
+        for r, (hb, o) in enumerate(allh):
+            if r == self.rank:
+                out.append(ptr)
+                continue
+            p = ctypes.c_void_p()
+            _lib.call("fq_ipc_open", hb, o, ctypes.byref(p))
+            out.append(p.value)
+            self._opened.append((p.value, o))
+        return out
+
+    def _barrier(self) -> None:
+        """Order this rank's stream against every rank's: a stream-ordered
+        flag barrier in peer memory (fq_peer_barrier, no host sync), or host
+        synchronisation + dist.barrier."""
+        if self.device_barrier:
             import ctypes
 
-            self._p2p_buf = self.ops.empty(self.n_local)
-            h = (ctypes.c_char * 64)()
-            off = ctypes.c_int64()
-            _lib.call("fq_ipc_handle", self._p2p_buf.data_ptr(), h, ctypes.byref(off))
-            mine = (bytes(h), off.value)
-            allh = [None] * self.K
-            dist.all_gather_object(allh, mine, group=self.group)
-            peers = []
-            for r, (hb, o) in enumerate(allh):
-                if r == self.rank:
-                    peers.append(self._p2p_buf.data_ptr())
-                    continue
-                ptr = ctypes.c_void_p()
-                _lib.call("fq_ipc_open", hb, o, ctypes.byref(ptr))
-                peers.append(ptr.value)
-                self._opened.append((ptr.value, o))
-            self._peers = peers
-        return self._p2p_buf
+            self._epoch += 1
+            ptrs = (ctypes.c_void_p * self.K)(*self._flag_ptrs)
+            _lib.call("fq_peer_barrier", ptrs, self.K, self.rank, self._epoch,
+                      self._flags.data_ptr() + 4 * self.K, _lib.stream())
+        else:
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+
+    def check_barrier(self) -> None:
+        if self._p2p_buf is not None and self.device_barrier and int(self._flags[self.K].item()) != 0:
+            raise RuntimeError("peer barrier timed out (a rank did not arrive)")
 
     def _global_p2p(self, us: Sequence[SU2]) -> None:
         """Alg. 4's exchange -> k-position pass -> exchange as ONE peer-memory
@@ -498,11 +527,9 @@ class ShardedQaoaSimulator:
         indices of its 1/K part across all K shards, in place.  Two barriers
         order it against every rank's local passes.  Logical exchange count
         as in the reference (2 per layer)."""
-        torch.cuda.synchronize()
-        dist.barrier(group=self.group)
+        self._barrier()
         global_su2_pass(self._peers, self.k, 1 << self.n_local, self.rank, self.K, us)
-        torch.cuda.synchronize()
-        dist.barrier(group=self.group)
+        self._barrier()
         self.exchange_count += 2
         instrumentation.bump("exchange", 2)
 
@@ -554,6 +581,7 @@ class ShardedQaoaSimulator:
         return self.expectation() if expectation else None
 
     def expectation(self) -> float:
+        self.check_barrier()
         local = self.ops.expectation(self._state, self.costs)
         dist.all_reduce(local, op=dist.ReduceOp.SUM, group=self.group)
         return float(local.item())

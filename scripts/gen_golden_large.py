@@ -63,6 +63,8 @@ CASES = {
     "port22_ring_p2": (lambda: portfolio(22), "xy-ring", 2, bench_angles, 11),
     "port22_complete_p1": (lambda: portfolio(22), "xy-complete", 1, bench_angles, 11),
     "port26_ring_p1": (lambda: portfolio(26), "xy-ring", 1, bench_angles, 13),
+    # BASELINE config 3's size (the reference's n <= 30 limit): ~15 min on 8 cores, mostly precompute
+    "labs30_x_p3": (lambda: labs_terms(30), "x", 3, bench_angles, None),
 }
 
 

@@ -32,7 +32,7 @@ def _mixer(kind, n):
                                       for j in range(n)])
 
 
-def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange"):
+def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange", dev_barrier=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -44,7 +44,8 @@ def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange"):
         rng = np.random.default_rng(11)
         g, b = rng.uniform(0, 1, p), rng.uniform(0, 1, p)
         poly = labs_terms(n) if kind in ("x", "custom") else portfolio_terms(n)
-        sim = ShardedQaoaSimulator(poly, mixer=_mixer(kind, n), chunk_bytes=chunk, global_mode=mode)
+        sim = ShardedQaoaSimulator(poly, mixer=_mixer(kind, n), chunk_bytes=chunk, global_mode=mode,
+                                   device_barrier=dev_barrier)
         E = sim.simulate_qaoa(g, b, initial_weight=n // 2 if kind.startswith("xy") else None)
         ov = sim.overlap()
         q.put((rank, E, ov, sim.exchange_count, sim.shard.cpu().numpy()))
@@ -55,11 +56,12 @@ def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,p,kind,chunk,mode", [(16, 3, "x", None, "exchange"), (17, 2, "x", 1 << 16, "exchange"),
-                                                 (14, 2, "xy-ring", None, "exchange"), (16, 3, "x", None, "p2p"),
-                                                 (19, 2, "x", None, "p2p"), (15, 2, "custom", None, "p2p"),
-                                                 (15, 2, "custom", None, "exchange")])
-def test_two_process_sharded_matches_single_gpu(n, p, kind, chunk, mode):
+@pytest.mark.parametrize("n,p,kind,chunk,mode,dev_barrier",
+                         [(16, 3, "x", None, "exchange", True), (17, 2, "x", 1 << 16, "exchange", True),
+                          (14, 2, "xy-ring", None, "exchange", True), (16, 3, "x", None, "p2p", True),
+                          (19, 2, "x", None, "p2p", False), (15, 2, "custom", None, "p2p", True),
+                          (15, 2, "custom", None, "exchange", True)])
+def test_two_process_sharded_matches_single_gpu(n, p, kind, chunk, mode, dev_barrier):
     from oracle import oracle as O
     from paper_2309_04841_b200 import Mixer, QaoaSimulator, hamming_weight_state
     from paper_2309_04841_b200.problems import labs_terms, portfolio_terms
@@ -68,7 +70,8 @@ def test_two_process_sharded_matches_single_gpu(n, p, kind, chunk, mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, p, kind, chunk, q, mode)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, p, kind, chunk, q, mode, dev_barrier))
+             for r in range(world)]
     for pr in procs:
         pr.start()
     out = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
