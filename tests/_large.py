@@ -26,6 +26,7 @@ CASES = {
     "port22_ring_p2": (lambda: portfolio_terms(22), "xy-ring", 11),
     "port22_complete_p1": (lambda: portfolio_terms(22), "xy-complete", 11),
     "port26_ring_p1": (lambda: portfolio_terms(26), "xy-ring", 13),
+    "labs30_x_p3": (lambda: labs_terms(30), "x", None),  # BASELINE config 3's size, the reference's n <= 30 limit
 }
 
 
