@@ -41,12 +41,26 @@ def _headers() -> list[str]:
         [os.path.join(INCLUDE, "fqaoa.h"), __file__]
 
 
+STAMP = LIB + ".stamp"
+
+
+def _digest() -> str:
+    """Content hash of every build input (robust to mtime changes when the
+    tree is copied, e.g. to the GPU box)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for path in sorted([os.path.join(CSRC, f) for f in SOURCES] + _headers()):
+        with open(path, "rb") as f:
+            h.update(os.path.basename(path).encode() + b"\0" + f.read())
+    return h.hexdigest()
+
+
 def _stale() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES] + _headers()
-    return any(os.path.getmtime(d) > t for d in deps)
+    with open(STAMP) as f:
+        return f.read().strip() != _digest()
 
 
 def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
@@ -100,6 +114,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
     os.replace(tmp_lib, LIB)
+    with open(STAMP, "w") as f:
+        f.write(_digest() + "\n")
     return LIB
 
 
