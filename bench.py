@@ -189,6 +189,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--global-mode", default="p2p", choices=["p2p", "exchange"],
                     help="N>1: global-qubit mixer as one peer-memory kernel (p2p) or NCCL all-to-all exchanges")
+    ap.add_argument("--state", default="c128", choices=["c128", "c64"],
+                    help="state type: complex128 (the headline, the reference's) or the optional complex64 (N=1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -233,8 +235,11 @@ def main():
     barrier()
     t0 = time.perf_counter()
     poly = labs_terms(n)
+    c64 = args.state == "c64"
+    if c64 and world > 1:
+        raise SystemExit("--state c64 is a single-GPU option")
     if world == 1:
-        sim = QaoaSimulator(terms=poly)
+        sim = QaoaSimulator(terms=poly, dtype=torch.complex64 if c64 else torch.complex128)
         dc = sim.device_costs
     else:
         sim = ShardedQaoaSimulator(poly, global_mode=args.global_mode)
@@ -242,13 +247,13 @@ def main():
     barrier()
     precompute_s = time.perf_counter() - t0
     n_local = n - k
-    S = 16 * (1 << n_local)
+    S = (8 if c64 else 16) * (1 << n_local)
     Cb = dc.nbytes_per_amp() * (1 << n_local)
 
     # ------------------------------------------------------------ device-resident step
     layers = [(float(gi), float(bi), 1, 0, n_local) for gi, bi in zip(g, b)]
     if world == 1:
-        state = torch.empty(1 << n, dtype=torch.complex128, device="cuda")
+        state = torch.empty(1 << n, dtype=torch.complex64 if c64 else torch.complex128, device="cuda")
         exp_dev = torch.empty(1, dtype=torch.float64, device="cuda")
         amp = 1.0 / math.sqrt(float(1 << n))
 
@@ -339,7 +344,7 @@ def main():
         try:
             with open(tp) as f:
                 tj = json.load(f)
-            if tj.get("n") == n_local:
+            if tj.get("n") == n_local and tj.get("state", "c128") == args.state:
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
@@ -347,6 +352,8 @@ def main():
     # ------------------------------------------------------------ e2e through the public API
     e2e = None
     if world == 1:
+        objective = float(exp_dev.item())
+        del step, state  # the API allocates its own state (n = 34 complex64: no room for two)
         rng = np.random.default_rng(1)
         sets = [(g + 1e-3 * rng.standard_normal(p), b + 1e-3 * rng.standard_normal(p))
                 for _ in range(args.steps + args.warmup)]
@@ -396,26 +403,27 @@ def main():
                          f"oracle C/OpenMP port, extrapolated to the p={p} evaluation "
                          f"({1e3 * t_layer:.0f} ms/layer, {1e3 * t_exp:.0f} ms expectation)"}
 
-    objective = float(exp_dev.item()) if world == 1 else float(sim.expectation())  # collective for N > 1
+    if world > 1:
+        objective = float(sim.expectation())  # collective
     if rank == 0:
         line = {
             **({"validation_only": "all ranks on one GPU (FQ_BENCH_ONE_DEVICE)"} if one_device else {}),
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": f"LABS n={n} p={p} X-mixer complex128 objective evaluation"
+            "vs_baseline": None, "dtype": args.state, "data": "synthetic",
+            "config": {"workload": f"LABS n={n} p={p} X-mixer {'complex64' if c64 else 'complex128'} objective evaluation"
                                    + (f" sharded over {world} GPUs (n_local={n_local}; value in n=26-equivalent "
                                       f"evaluations)" if world > 1 else ""),
                        "n": n, "p": p, "n_local": n_local, "angles": "default_rng(0) U(0,1)",
                        "cost_encoding": "uint16 levels (lossless)" if dc.u16 is not None else "float64",
-                       "l2": "no flush: 1 GiB state per GPU >> 126 MB L2",
+                       "l2": f"no flush: {S / 2**30:.1f} GiB state per GPU >> 126 MB L2",
                        "parallelism": (f"state sharded over {world} GPUs by global qubits, global-qubit mixer: "
                                        f"{'peer-memory kernel (CUDA IPC over NVLink)' if args.global_mode == 'p2p' else 'NCCL all-to-all'}")
                                       if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                          "kernel": "k_pass16 (every tiled pass of the step; per-launch CUDA events)",
-                         "bytes_per_launch": "2*S + C(phase/expectation) - S(|+> generated); S = 16*2^n, "
+                         "bytes_per_launch": f"2*S + C(phase/expectation) - S(|+> generated); S = {S >> n_local}*2^n, "
                                              "C = cost bytes per amplitude * 2^n",
                          "achieved_whole_step": achieved_step,
                          "algorithmic_bytes_per_step": tile_bytes, "passes_per_step": passes if world == 1 else None,

@@ -44,6 +44,10 @@ extern "C" {
 #define FQ_COST_F64 0 /* double per amplitude (terms.py:102-120 output)       */
 #define FQ_COST_U16 1 /* uint16 level v, cost = scale*v + offset (terms.py:123-175) */
 
+/* state element types (fq_evolve_desc.state_kind) */
+#define FQ_STATE_C128 0 /* complex128: the reference's state (default)        */
+#define FQ_STATE_C64 1  /* complex64: optional single-precision state         */
+
 int fq_version(void);
 const char *fq_last_error(void);
 /* Number of SMs of the current device (grid sizing), or -1. */
@@ -133,6 +137,19 @@ int fq_masked_probability(const void *psi, const void *costs, int cost_kind, dou
                           double offset, int64_t size, double cutoff, double *out_dev,
                           double *scratch, void *stream);
 
+/* complex64 states (an optional single-precision path the reference does not
+ * have; north star: "complex128, with complex64 optional", 1e-4 tolerance):
+ * the same operations on interleaved float re/im.  Observables accumulate
+ * in fp64. */
+int fq_init_state_c64(void *psi, int64_t size, int weight, double amp, int64_t index_base,
+                      void *stream);
+int fq_abs2_inplace_c64(void *psi, int64_t size, void *stream);
+int fq_expectation_c64(const void *psi, const void *costs, int cost_kind, double scale,
+                       double offset, int64_t size, double *out_dev, double *scratch, void *stream);
+int fq_masked_probability_c64(const void *psi, const void *costs, int cost_kind, double scale,
+                              double offset, int64_t size, double cutoff, double *out_dev,
+                              double *scratch, void *stream);
+
 /* Lossless uint16 packing of a float64 diagonal (terms.py:155-175):
  * out[k] = rint((c_k - offset)/scale); *bad_dev set nonzero if any level > 65535 or
  * scale*v + offset != c_k bit-for-bit. */
@@ -171,6 +188,8 @@ typedef struct fq_evolve_desc {
     double init_amp;      /* amplitude used when init == 1 (reference: 1/sqrt(2^n_global)) */
     double *expectation_dev;  /* if non-NULL: sum_k c_k |psi_k|^2 of the final state  */
     double *scratch;      /* device, >= FQ_SCRATCH_DOUBLES doubles                   */
+    int state_kind;       /* FQ_STATE_C128 (default, zero) / FQ_STATE_C64: psi is
+                             complex64[2^n]; X mixer, n > 12 (tiled passes)          */
 } fq_evolve_desc;
 
 /* Runs the whole p-layer program: phase fused into the first mixer pass of

@@ -20,6 +20,7 @@ FQ_OK, FQ_ERR_ARG, FQ_ERR_CUDA, FQ_ERR_UNSUPPORTED = 0, 1, 2, 3
 FQ_SCRATCH_DOUBLES = 4096
 MIXER_CODES = {"x": 0, "xy-ring": 1, "xy-complete": 2, "custom": 3}
 COST_F64, COST_U16 = 0, 1
+STATE_C128, STATE_C64 = 0, 1
 
 P, I64, D, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
 
@@ -32,7 +33,7 @@ class FqEvolveDesc(ctypes.Structure):
     _fields_ = [
         ("psi", P), ("n", I), ("cost_kind", I), ("costs", P), ("cost_scale", D), ("cost_offset", D),
         ("cost_levels", I), ("mixer", I), ("n_layers", I), ("layers", ctypes.POINTER(FqLayer)), ("su2", ctypes.POINTER(D)),
-        ("init", I), ("init_amp", D), ("expectation_dev", P), ("scratch", P),
+        ("init", I), ("init_amp", D), ("expectation_dev", P), ("scratch", P), ("state_kind", I),
     ]
 
 
@@ -51,6 +52,10 @@ _SIGS = {
     "fq_abs2_inplace": ([P, I64, P], I),
     "fq_init_state": ([P, I64, I, D, I64, P], I),
     "fq_expectation": ([P, P, I, D, D, I64, P, P, P], I),
+    "fq_init_state_c64": ([P, I64, I, D, I64, P], I),
+    "fq_abs2_inplace_c64": ([P, I64, P], I),
+    "fq_expectation_c64": ([P, P, I, D, D, I64, P, P, P], I),
+    "fq_masked_probability_c64": ([P, P, I, D, D, I64, D, P, P, P], I),
     "fq_cost_minmax": ([P, I, D, D, I64, P, P, P], I),
     "fq_masked_probability": ([P, P, I, D, D, I64, D, P, P, P], I),
     "fq_compact_u16": ([P, P, I64, D, D, P, P], I),

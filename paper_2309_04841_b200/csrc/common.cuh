@@ -34,6 +34,9 @@ inline int log2i(int64_t x) { int r = 0; while ((int64_t(1) << r) < x) ++r; retu
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
 
 // Decode of a uint16 level exactly as the reference's CompactCostVector.decode
 // (terms.py:133-135: scale * v + offset, two roundings, never contracted to FMA).
@@ -44,6 +47,8 @@ __device__ __forceinline__ double decode_u16(uint16_t v, double scale, double of
 // streaming (evict-first) 16-B global accesses: each amplitude is touched once per pass
 __device__ __forceinline__ double2 ld_stream(const double2 *p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stcs(p, v); }
+__device__ __forceinline__ float2 ld_stream(const float2 *p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(float2 *p, float2 v) { __stcs(p, v); }
 
 // Deterministic block reduction (fixed shuffle tree + fixed smem order).
 template <int NT>

@@ -155,21 +155,50 @@ __global__ void __launch_bounds__(kResThreads) k_resident(const __grid_constant_
 }
 
 // ---------------------------------------------------------------- standalone phase (uint16)
-__global__ void k_phase_u16(double2 *__restrict__ psi, const uint16_t *__restrict__ lv, long long size, double gamma,
+// T = double2 (complex128 states) or float2 (complex64); the angle is always fp64
+template <typename T>
+__global__ void k_phase_u16(T *__restrict__ psi, const uint16_t *__restrict__ lv, long long size, double gamma,
                             double scale, double offset) {
+    using R = decltype(T::x);
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < size;
-         k += (long long)gridDim.x * blockDim.x)
-        psi[k] = cmul(psi[k], phase_f64(decode_u16(lv[k], scale, offset), gamma));
+         k += (long long)gridDim.x * blockDim.x) {
+        const double2 f = phase_f64(decode_u16(lv[k], scale, offset), gamma);
+        psi[k] = cmul(psi[k], T{(R)f.x, (R)f.y});
+    }
 }
 
-__global__ void k_phase_f64(double2 *__restrict__ psi, const double *__restrict__ costs, long long size,
-                            double gamma) {
+template <typename T>
+__global__ void k_phase_f64(T *__restrict__ psi, const double *__restrict__ costs, long long size, double gamma) {
+    using R = decltype(T::x);
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < size;
          k += (long long)gridDim.x * blockDim.x) {
         double s, c;
         sincos(gamma * costs[k], &s, &c);
-        psi[k] = cmul(psi[k], make_double2(c, -s));
+        psi[k] = cmul(psi[k], T{(R)c, (R)-s});
     }
+}
+
+// standalone phase / state init / expectation on either state type
+template <typename T>
+static void launch_phase(T *psi, const fq_evolve_desc *d, long long size, double gamma, cudaStream_t st) {
+    if (d->cost_kind == FQ_COST_U16)
+        k_phase_u16<<<grid_for(size, 256, 8), 256, 0, st>>>(psi, static_cast<const uint16_t *>(d->costs), size, gamma,
+                                                            d->cost_scale, d->cost_offset);
+    else
+        k_phase_f64<<<grid_for(size, 256, 8), 256, 0, st>>>(psi, static_cast<const double *>(d->costs), size, gamma);
+}
+
+static int state_init(const fq_evolve_desc *d, void *psi, long long size, cudaStream_t st) {
+    return d->state_kind == FQ_STATE_C64 ? fq_init_state_c64(psi, size, -1, d->init_amp, 0, st)
+                                         : fq_init_state(psi, size, -1, d->init_amp, 0, st);
+}
+
+static int state_expectation(const fq_evolve_desc *d, const void *psi, long long size, cudaStream_t st) {
+    return d->state_kind == FQ_STATE_C64
+               ? fq_expectation_c64(psi, d->costs, d->cost_kind, d->cost_scale, d->cost_offset, size,
+                                    d->expectation_dev, d->scratch, st)
+               : fq_expectation(psi, d->costs, d->cost_kind, d->cost_scale, d->cost_offset, size, d->expectation_dev,
+                                d->scratch, st);
 }
 
 // ---------------------------------------------------------------- host planning
@@ -381,11 +410,14 @@ static int mask_class(int seq, const unsigned char *maskA) {
 
 // RX forms are compile-time for set A and for set B of heavy passes (set B of
 // a light pass runs in the run-time form: it only occurs for gamma = 0 layers).
-static int launch_pass(int mix, int cost, const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb,
-                       int grid, cudaStream_t st) {
+static int launch_pass(int mix, int cost, bool c64, const PassParams &P, const PassMaps &M, int seq, int ph, int ma,
+                       int mb, int grid, cudaStream_t st) {
     const int k = mask_class(seq, P.maskA);
     if (mix == MIX_SU2) return launch_pass_su2(P, M, cost, seq, ph, mb == 2 ? 2 : 3, k, grid, st);
     if (!seq_heavy(seq) && mb != 2) mb = 3;
+    if (c64)
+        return cost == FQ_COST_U16 ? launch_pass_c64_u16(P, M, seq, ph, ma, mb, k, grid, st)
+                                   : launch_pass_c64_f64(P, M, seq, ph, ma, mb, k, grid, st);
     if (cost == FQ_COST_U16)
         return seq_heavy(seq) ? launch_pass_rx_u16_heavy(P, M, seq, ph, ma, mb, k, grid, st)
                               : launch_pass_rx_u16_light(P, M, seq, ph, ma, mb, k, grid, st);
@@ -405,19 +437,19 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
         table_hi = rows <= kMaxTableHi ? rows : 0;
     }
     bool init_pending = d->init != 0;
-    double2 *psi = static_cast<double2 *>(d->psi);
+    const bool c64 = d->state_kind == FQ_STATE_C64;
+    const long long elem = c64 ? (long long)sizeof(float2) : (long long)sizeof(double2);
+    void *psi = d->psi;
     const long long size = 1LL << n;
     const int sms = sm_count() > 0 ? sm_count() : 148;
     const int grid = (int)std::min<long long>(n_tiles, (long long)sms * 2);
 
     if (seq.empty()) {
         if (init_pending) {
-            int s = fq_init_state(psi, size, -1, d->init_amp, 0, st);
+            int s = state_init(d, psi, size, st);
             if (s) return s;
         }
-        if (d->expectation_dev)
-            return fq_expectation(psi, d->costs, d->cost_kind, d->cost_scale, d->cost_offset, size,
-                                  d->expectation_dev, d->scratch, st);
+        if (d->expectation_dev) return state_expectation(d, psi, size, st);
         return FQ_OK;
     }
     g_last_plan.clear();
@@ -438,21 +470,16 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
         if (pp.group < 0) {  // standalone phase
             g_last_plan.push_back({-1, 1, 0, init_pending ? 1 : 0, (last && d->expectation_dev) ? 1 : 0});
             if (init_pending) {
-                int s = fq_init_state(psi, size, -1, d->init_amp, 0, st);
+                int s = state_init(d, psi, size, st);
                 if (s) return s;
                 init_pending = false;
             }
             const fq_layer &L = d->layers[pp.phase_layer];
-            if (d->cost_kind == FQ_COST_U16)
-                k_phase_u16<<<grid_for(size, 256, 8), 256, 0, st>>>(psi, static_cast<const uint16_t *>(d->costs), size,
-                                                                    L.gamma, d->cost_scale, d->cost_offset);
-            else
-                k_phase_f64<<<grid_for(size, 256, 8), 256, 0, st>>>(psi, static_cast<const double *>(d->costs), size,
-                                                                    L.gamma);
+            if (c64) launch_phase(static_cast<float2 *>(psi), d, size, L.gamma, st);
+            else launch_phase(static_cast<double2 *>(psi), d, size, L.gamma, st);
             FQ_LAUNCHED("k_phase");
             if (last && d->expectation_dev) {
-                int s = fq_expectation(psi, d->costs, d->cost_kind, d->cost_scale, d->cost_offset, size,
-                                       d->expectation_dev, d->scratch, st);
+                int s = state_expectation(d, psi, size, st);
                 if (s) return s;
             }
             if (int s = mark(si + 1)) return s;
@@ -476,7 +503,7 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
                 long long o = 0;
                 for (int j = 0; j < 4; ++j)
                     if ((i >> j) & 1) o += 1LL << g.tile_pos[f + j];
-                P.roff[pat][i] = o * (long long)sizeof(double2);
+                P.roff[pat][i] = o * elem;
                 P.coff[pat][i] = o * (d->cost_kind == FQ_COST_F64 ? 8 : 2);
             }
         }
@@ -524,8 +551,10 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
         PassMaps M;
         std::memset(&M, 0, sizeof M);
         if (P.pf_dist > 0) {
-            P.sm_rank = cached_tile_map(&M.state, psi, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2, P.sm_shift,
-                                       P.sm_bits);
+            P.sm_rank = c64 ? cached_tile_map(&M.state, psi, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 2,
+                                              P.sm_shift, P.sm_bits)
+                            : cached_tile_map(&M.state, psi, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2,
+                                              P.sm_shift, P.sm_bits);
             if (P.pf_cost)
                 P.cm_rank = d->cost_kind == FQ_COST_F64
                                 ? cached_tile_map(&M.cost, d->costs, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 1,
@@ -536,7 +565,7 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
         }
         const int ma = P.A.mode, mb = two ? P.B.mode : 2;
         if (P.expect && ph == 0 && !two && !seq_heavy(sq)) ph = 3;  // preload the expectation's costs
-        const int s = launch_pass(mix, d->cost_kind, P, M, sq, ph, ma, mb, grid, st);
+        const int s = launch_pass(mix, d->cost_kind, c64, P, M, sq, ph, ma, mb, grid, st);
         if (s) return s;
         g_last_plan.push_back({sq, ph, (int)g.targets.size(), P.init, P.expect});
         if (P.expect) {
@@ -704,6 +733,12 @@ int fq_qaoa_evolve(const fq_evolve_desc *d, void *stream) {
     FQ_CHECK_ARG(d->mixer >= FQ_MIXER_X && d->mixer <= FQ_MIXER_CUSTOM, "fq_qaoa_evolve: bad mixer");
     FQ_CHECK_ARG(d->mixer != FQ_MIXER_CUSTOM || d->su2, "fq_qaoa_evolve: custom mixer needs su2 table");
     FQ_CHECK_ARG(!d->expectation_dev || d->scratch, "fq_qaoa_evolve: expectation needs scratch");
+    FQ_CHECK_ARG(d->state_kind == FQ_STATE_C128 || d->state_kind == FQ_STATE_C64, "fq_qaoa_evolve: bad state kind");
+    if (d->state_kind == FQ_STATE_C64 && (d->n <= kTileBits || d->mixer != FQ_MIXER_X)) {
+        set_error("fq_qaoa_evolve: complex64 states run the X mixer on n > %d qubits (got n=%d, mixer=%d)", kTileBits,
+                  d->n, d->mixer);
+        return FQ_ERR_UNSUPPORTED;
+    }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (d->n <= kTileBits) {
         FQ_CHECK_ARG(d->mixer != FQ_MIXER_CUSTOM || d->scratch, "fq_qaoa_evolve: custom mixer needs scratch");

@@ -121,6 +121,15 @@ __global__ void k_abs2(double2 *__restrict__ psi, int64_t size) {
     }
 }
 
+// complex64 states: same two roundings in single precision
+__global__ void k_abs2_c64(float2 *__restrict__ psi, int64_t size) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < size;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const float2 x = psi[k];
+        psi[k] = make_float2(__fadd_rn(__fmul_rn(x.x, x.x), __fmul_rn(x.y, x.y)), 0.0f);
+    }
+}
+
 // ------------------------------------------------------------ precompute
 // Terms are staged through shared memory in chunks; every thread walks the
 // chunk in term order for its own elements (reference _kernels.py:81-94:
@@ -238,12 +247,12 @@ __global__ void __launch_bounds__(kPreThreads) k_accumulate_int(void *__restrict
 }
 
 // ------------------------------------------------------------ states
-__global__ void k_init_state(double2 *__restrict__ psi, int64_t size, int weight, double amp,
-                             int64_t base) {
+template <typename T>
+__global__ void k_init_state(T *__restrict__ psi, int64_t size, int weight, double amp, int64_t base) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < size;
          k += (int64_t)gridDim.x * blockDim.x) {
         const bool on = weight < 0 || __popcll((unsigned long long)(base + k)) == weight;
-        psi[k] = make_double2(on ? amp : 0.0, 0.0);
+        psi[k] = {on ? (decltype(T::x))amp : (decltype(T::x))0, (decltype(T::x))0};
     }
 }
 
@@ -257,8 +266,9 @@ __device__ __forceinline__ double load_cost(const void *costs, int64_t k, double
 constexpr int kRedThreads = 256;
 
 // OP 0: sum c|x|^2 ; OP 1: sum_{c <= cutoff} |x|^2 ; OP 2: min c ; OP 3: max c
-template <int KIND, int OP>
-__global__ void __launch_bounds__(kRedThreads) k_reduce(const double2 *__restrict__ psi, const void *costs,
+// T: double2 (complex128 states) or float2 (complex64 states; accumulated in fp64)
+template <int KIND, int OP, typename T>
+__global__ void __launch_bounds__(kRedThreads) k_reduce(const T *__restrict__ psi, const void *costs,
                                                         double scale, double offset, int64_t size,
                                                         double cutoff, double *partials) {
     __shared__ double red[kRedThreads / 32];
@@ -267,12 +277,12 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce(const double2 *__restric
          k += (int64_t)gridDim.x * blockDim.x) {
         const double c = load_cost<KIND>(costs, k, scale, offset);
         if (OP == 0) {
-            const double2 x = psi[k];
-            acc += c * (x.x * x.x + x.y * x.y);
+            const T x = psi[k];
+            acc += c * ((double)x.x * x.x + (double)x.y * x.y);
         } else if (OP == 1) {
             if (c <= cutoff) {
-                const double2 x = psi[k];
-                acc += x.x * x.x + x.y * x.y;
+                const T x = psi[k];
+                acc += (double)x.x * x.x + (double)x.y * x.y;
             }
         } else if (OP == 2) {
             acc = fmin(acc, c);
@@ -331,7 +341,16 @@ static inline cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
 
 template <int OP>
 static int launch_reduce(const void *psi, const void *costs, int kind, double scale, double offset,
-                         int64_t size, double cutoff, double *partials, int grid, cudaStream_t st) {
+                         int64_t size, double cutoff, double *partials, int grid, cudaStream_t st, bool c64 = false) {
+    if (c64) {
+        const float2 *p = static_cast<const float2 *>(psi);
+        if (kind == FQ_COST_F64)
+            k_reduce<FQ_COST_F64, OP><<<grid, kRedThreads, 0, st>>>(p, costs, scale, offset, size, cutoff, partials);
+        else
+            k_reduce<FQ_COST_U16, OP><<<grid, kRedThreads, 0, st>>>(p, costs, scale, offset, size, cutoff, partials);
+        FQ_LAUNCHED("k_reduce");
+        return FQ_OK;
+    }
     const double2 *p = static_cast<const double2 *>(psi);
     if (kind == FQ_COST_F64)
         k_reduce<FQ_COST_F64, OP><<<grid, kRedThreads, 0, st>>>(p, costs, scale, offset, size, cutoff, partials);
@@ -488,6 +507,45 @@ int fq_masked_probability(const void *psi, const void *costs, int cost_kind, dou
     FQ_CHECK_ARG(psi && costs && out_dev && scratch && size > 0, "fq_masked_probability: bad args");
     const int g = reduce_grid(size);
     int s = launch_reduce<1>(psi, costs, cost_kind, scale, offset, size, cutoff, scratch, g, S(stream));
+    if (s) return s;
+    k_sum_partials<<<1, 32, 0, S(stream)>>>(scratch, g, out_dev);
+    FQ_LAUNCHED("k_sum_partials");
+    return FQ_OK;
+}
+
+// ---- complex64 states (optional single-precision path; observables accumulate in fp64)
+int fq_init_state_c64(void *psi, int64_t size, int weight, double amp, int64_t index_base, void *stream) {
+    FQ_CHECK_ARG(psi && size > 0, "fq_init_state_c64: bad buffer");
+    k_init_state<<<grid_for(size, 256, 8), 256, 0, S(stream)>>>(static_cast<float2 *>(psi), size, weight, amp,
+                                                                 index_base);
+    FQ_LAUNCHED("k_init_state");
+    return FQ_OK;
+}
+
+int fq_abs2_inplace_c64(void *psi, int64_t size, void *stream) {
+    FQ_CHECK_ARG(psi && size > 0, "fq_abs2_inplace_c64: bad buffer");
+    k_abs2_c64<<<grid_for(size, 256, 8), 256, 0, S(stream)>>>(static_cast<float2 *>(psi), size);
+    FQ_LAUNCHED("k_abs2");
+    return FQ_OK;
+}
+
+int fq_expectation_c64(const void *psi, const void *costs, int cost_kind, double scale, double offset,
+                       int64_t size, double *out_dev, double *scratch, void *stream) {
+    FQ_CHECK_ARG(psi && costs && out_dev && scratch && size > 0, "fq_expectation_c64: bad args");
+    FQ_CHECK_ARG(cost_kind == FQ_COST_F64 || cost_kind == FQ_COST_U16, "fq_expectation_c64: bad cost kind");
+    const int g = reduce_grid(size);
+    int s = launch_reduce<0>(psi, costs, cost_kind, scale, offset, size, 0.0, scratch, g, S(stream), true);
+    if (s) return s;
+    k_sum_partials<<<1, 32, 0, S(stream)>>>(scratch, g, out_dev);
+    FQ_LAUNCHED("k_sum_partials");
+    return FQ_OK;
+}
+
+int fq_masked_probability_c64(const void *psi, const void *costs, int cost_kind, double scale, double offset,
+                              int64_t size, double cutoff, double *out_dev, double *scratch, void *stream) {
+    FQ_CHECK_ARG(psi && costs && out_dev && scratch && size > 0, "fq_masked_probability_c64: bad args");
+    const int g = reduce_grid(size);
+    int s = launch_reduce<1>(psi, costs, cost_kind, scale, offset, size, cutoff, scratch, g, S(stream), true);
     if (s) return s;
     k_sum_partials<<<1, 32, 0, S(stream)>>>(scratch, g, out_dev);
     FQ_LAUNCHED("k_sum_partials");

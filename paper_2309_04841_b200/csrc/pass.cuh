@@ -21,6 +21,21 @@ constexpr int kThreads = 256;
 constexpr int kRegs = 16;
 
 enum { MIX_RX = 0, MIX_SU2 = 1 };
+
+// State precision: R = double (complex128, the reference's) or float
+// (complex64, optional).  C2<R> is the interleaved complex element.
+template <typename R> struct Cx;
+template <> struct Cx<double> {
+    using T = double2;
+    static __host__ __device__ __forceinline__ double2 make(double x, double y) { return make_double2(x, y); }
+};
+template <> struct Cx<float> {
+    using T = float2;
+    static __host__ __device__ __forceinline__ float2 make(float x, float y) { return make_float2(x, y); }
+};
+template <typename R> using C2 = typename Cx<R>::T;
+// phase-table copies: one per bank group of the access width (16 B: 8 per 128 B, 8 B: 16)
+template <typename R> constexpr int table_copies() { return 128 / (int)sizeof(C2<R>); }
 enum { PAT8 = 0, PAT0 = 1, PAT4 = 2 };  // tile bits held in registers: 8-11 / 0-3 / 4-7
 
 // Round programs (register patterns visited by one pass):
@@ -49,7 +64,7 @@ struct CoefSet {
 };
 
 struct PassParams {
-    double2 *psi;
+    void *psi;                // C2<R>[2^n]
     const void *costs;
     double cost_scale, cost_offset;
     double *partials;
@@ -119,54 +134,57 @@ __device__ __forceinline__ long long thread_offset(const PassParams &P, int tid)
     return off;
 }
 
-template <int FROM, int TO>
-__device__ __forceinline__ void transpose(double2 *sm, double2 (&v)[kRegs], int tid) {
-    double2 *p = sm + pat_base<FROM>(tid);
+template <int FROM, int TO, typename T>
+__device__ __forceinline__ void transpose(T *sm, T (&v)[kRegs], int tid) {
+    T *p = sm + pat_base<FROM>(tid);
 #pragma unroll
     for (int i = 0; i < kRegs; ++i) p[pat_step<FROM>(i)] = v[i];
     __syncthreads();
-    const double2 *q = sm + pat_base<TO>(tid);
+    const T *q = sm + pat_base<TO>(tid);
 #pragma unroll
     for (int i = 0; i < kRegs; ++i) v[i] = q[pat_step<TO>(i)];
     __syncthreads();
 }
 
 // ---- butterflies
-__device__ __forceinline__ void bfly_rx0(double2 &x0, double2 &x1, double t) {
+template <typename T, typename R>
+__device__ __forceinline__ void bfly_rx0(T &x0, T &x1, R t) {
     // (x0 - i t x1, x1 - i t x0)
-    const double2 a = x0, b = x1;
-    x0 = make_double2(fma(t, b.y, a.x), fma(-t, b.x, a.y));
-    x1 = make_double2(fma(t, a.y, b.x), fma(-t, a.x, b.y));
+    const T a = x0, b = x1;
+    x0 = Cx<R>::make(fma(t, b.y, a.x), fma(-t, b.x, a.y));
+    x1 = Cx<R>::make(fma(t, a.y, b.x), fma(-t, a.x, b.y));
 }
-__device__ __forceinline__ void bfly_rx1(double2 &x0, double2 &x1, double u) {
+template <typename T, typename R>
+__device__ __forceinline__ void bfly_rx1(T &x0, T &x1, R u) {
     // (u x0 - i x1, u x1 - i x0)
-    const double2 a = x0, b = x1;
-    x0 = make_double2(fma(u, a.x, b.y), fma(u, a.y, -b.x));
-    x1 = make_double2(fma(u, b.x, a.y), fma(u, b.y, -a.x));
+    const T a = x0, b = x1;
+    x0 = Cx<R>::make(fma(u, a.x, b.y), fma(u, a.y, -b.x));
+    x1 = Cx<R>::make(fma(u, b.x, a.y), fma(u, b.y, -a.x));
 }
-__device__ __forceinline__ void bfly_su2(double2 &x0, double2 &x1, double2 a, double2 b) {
+template <typename T>
+__device__ __forceinline__ void bfly_su2(T &x0, T &x1, T a, T b) {
     // y0 = a x0 - conj(b) x1 ; y1 = b x0 + conj(a) x1   (reference _kernels.py:26-27)
-    const double2 p = x0, q = x1;
-    x0 = make_double2(a.x * p.x - a.y * p.y - b.x * q.x - b.y * q.y,
-                      a.x * p.y + a.y * p.x - b.x * q.y + b.y * q.x);
-    x1 = make_double2(b.x * p.x - b.y * p.y + a.x * q.x + a.y * q.y,
-                      b.x * p.y + b.y * p.x + a.x * q.y - a.y * q.x);
+    const T p = x0, q = x1;
+    x0.x = a.x * p.x - a.y * p.y - b.x * q.x - b.y * q.y;
+    x0.y = a.x * p.y + a.y * p.x - b.x * q.y + b.y * q.x;
+    x1.x = b.x * p.x - b.y * p.y + a.x * q.x + a.y * q.y;
+    x1.y = b.x * p.y + b.y * p.x + a.x * q.y - a.y * q.x;
 }
 
 // Butterflies of one coefficient set on the register bits in `mask`.
 // M: RX form 0 -> (1, t), 1 -> (u, 1), 3 -> chosen at run time.
-template <int MIX, int M, int PAT>
-__device__ __forceinline__ void bfly16(double2 (&v)[kRegs], const CoefSet &C, int mask) {
+template <int MIX, int M, int PAT, typename R>
+__device__ __forceinline__ void bfly16(C2<R> (&v)[kRegs], const CoefSet &C, int mask) {
     if (MIX == MIX_RX && M == 3) {
-        if (C.mode == 0) bfly16<MIX, 0, PAT>(v, C, mask);
-        else bfly16<MIX, 1, PAT>(v, C, mask);
+        if (C.mode == 0) bfly16<MIX, 0, PAT, R>(v, C, mask);
+        else bfly16<MIX, 1, PAT, R>(v, C, mask);
         return;
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         if (!((mask >> j) & 1)) continue;
         if (MIX == MIX_RX) {
-            const double r = C.r;
+            const R r = (R)C.r;
             if (M == 0) {
 #pragma unroll
                 for (int i = 0; i < kRegs; ++i)
@@ -178,7 +196,7 @@ __device__ __forceinline__ void bfly16(double2 (&v)[kRegs], const CoefSet &C, in
             }
         } else {
             const int tb = tile_bit_of_reg<PAT>(j);
-            const double2 a = C.a[tb], b = C.b[tb];
+            const C2<R> a = Cx<R>::make((R)C.a[tb].x, (R)C.a[tb].y), b = Cx<R>::make((R)C.b[tb].x, (R)C.b[tb].y);
 #pragma unroll
             for (int i = 0; i < kRegs; ++i)
                 if (!(i & (1 << j))) bfly_su2(v[i], v[i | (1 << j)], a, b);
@@ -221,30 +239,38 @@ __device__ __forceinline__ double decode_cost(const PassParams &P, CostRaw<COST>
 }
 
 // exp(-i gamma c): float64 -> sincos; uint16 level v -> T_hi[v >> 6] * T_lo[v & 63],
-// each table replicated once per 16-B bank group (copy = lane & 7) so a
-// quarter-warp's random lookups never conflict.
-template <int COST>
-__device__ __forceinline__ double2 phase16(const PassParams &P, CostRaw<COST> raw, const double2 *tlo,
-                                           const double2 *thi) {
+// each table replicated once per bank group of the access width (copy = lane
+// mod copies) so a (quarter- or half-) warp's random lookups never conflict.
+// Angles are reduced in double even for complex64 states (gamma * c reaches 1e3).
+template <int COST, typename R>
+__device__ __forceinline__ C2<R> phase16(const PassParams &P, CostRaw<COST> raw, const C2<R> *tlo,
+                                         const C2<R> *thi) {
     if constexpr (COST == FQ_COST_F64) {
-        return phase_f64(raw, P.gamma);
+        const double2 f = phase_f64(raw, P.gamma);
+        return Cx<R>::make((R)f.x, (R)f.y);
     } else {
-        if (P.table_hi == 0) return phase_sincos_u16(raw, P.cost_scale, P.cost_offset, P.gamma);
-        const int cp = threadIdx.x & (kCopies - 1);
-        return cmul(thi[(raw >> 6) * kCopies + cp], tlo[(raw & 63) * kCopies + cp]);
+        if (P.table_hi == 0) {
+            const double2 f = phase_sincos_u16(raw, P.cost_scale, P.cost_offset, P.gamma);
+            return Cx<R>::make((R)f.x, (R)f.y);
+        }
+        constexpr int CP = table_copies<R>();
+        const int cp = threadIdx.x & (CP - 1);
+        return cmul(thi[(raw >> 6) * CP + cp], tlo[(raw & 63) * CP + cp]);
     }
 }
 
 // e^{-i gamma c} tables for uint16 levels: c = scale*(64 h + l) + offset
-__device__ __forceinline__ void build_phase_tables(double2 *tlo, double2 *thi, int n_hi, double gamma, double scale,
+template <typename R>
+__device__ __forceinline__ void build_phase_tables(C2<R> *tlo, C2<R> *thi, int n_hi, double gamma, double scale,
                                                    double offset) {
+    constexpr int CP = table_copies<R>();
     for (int i = threadIdx.x; i < kTableLo + n_hi; i += blockDim.x) {
         double s, c;
         if (i < kTableLo) sincos(gamma * (scale * (double)i), &s, &c);
         else sincos(gamma * (scale * (double)(64 * (i - kTableLo)) + offset), &s, &c);
-        double2 *row = (i < kTableLo) ? tlo + i * kCopies : thi + (i - kTableLo) * kCopies;
+        C2<R> *row = (i < kTableLo) ? tlo + i * CP : thi + (i - kTableLo) * CP;
 #pragma unroll
-        for (int k = 0; k < kCopies; ++k) row[k] = make_double2(c, -s);
+        for (int k = 0; k < CP; ++k) row[k] = Cx<R>::make((R)c, (R)-s);
     }
 }
 
@@ -344,14 +370,15 @@ __device__ __forceinline__ int round_mask(const unsigned char *rt, int r) {
 //   K: target-mask class of the rounds (see round_mask): compile-time masks keep
 //       the butterfly code branch-free (run-time masks force register moves at
 //       every merge point).
-template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K>
+template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R = double>
 __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ PassParams P,
                                                         const __grid_constant__ CUtensorMap tm_state,
                                                         const __grid_constant__ CUtensorMap tm_cost) {
-    extern __shared__ double2 smem[];
-    double2 *tile = smem;
-    double2 *tlo = smem + kTilePadded;
-    double2 *thi = tlo + kTableLo * kCopies;
+    using T = C2<R>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *tile = reinterpret_cast<T *>(smem_raw);
+    T *tlo = tile + kTilePadded;
+    T *thi = tlo + kTableLo * table_copies<R>();
     __shared__ double red[kThreads / 32];
     const int tid = threadIdx.x;
     constexpr bool HAS_B = MB != 2;
@@ -363,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
     constexpr int LAST = seq_pat(SEQ, NR - 1);
 
     if (COST == FQ_COST_U16 && (PH == 1 || PH == 2)) {
-        if (P.table_hi > 0) build_phase_tables(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
+        if (P.table_hi > 0) build_phase_tables<R>(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
         __syncthreads();
     }
     const long long thr8 = thread_offset<PAT8>(P, tid);
@@ -389,16 +416,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
             if (tp < P.n_tiles) prefetch_tile(P, &tm_state, &tm_cost, P.reverse ? P.n_tiles - 1 - tp : tp, !P.init);
         }
         // per-tile base pointers; the registers' offsets are constant-bank byte offsets
-        const char *ps8 = reinterpret_cast<const char *>(P.psi + base + thr8);
+        const char *ps8 = reinterpret_cast<const char *>(static_cast<T *>(P.psi) + base + thr8);
         const char *cs = static_cast<const char *>(P.costs) + base * CB;
-        double2 v[kRegs];
+        T v[kRegs];
         CostRaw<COST> raw[kRegs];  // cost entries of the phase round, loaded with the state
         if (P.init) {
 #pragma unroll
-            for (int i = 0; i < kRegs; ++i) v[i] = make_double2(P.init_amp, 0.0);
+            for (int i = 0; i < kRegs; ++i) v[i] = Cx<R>::make((R)P.init_amp, (R)0);
         } else {
 #pragma unroll
-            for (int i = 0; i < kRegs; ++i) v[i] = ld_stream(reinterpret_cast<const double2 *>(ps8 + P.roff[PAT8][i]));
+            for (int i = 0; i < kRegs; ++i) v[i] = ld_stream(reinterpret_cast<const T *>(ps8 + P.roff[PAT8][i]));
         }
         if (PH == 1) {
             const char *c8 = cs + thr8 * CB;
@@ -427,61 +454,61 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
             if (P.probe & 4) return;
             if (P.probe & 2) {
 #pragma unroll
-                for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase16<COST>(P, (CostRaw<COST>)0, tlo, thi));
+                for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase16<COST, R>(P, (CostRaw<COST>)0, tlo, thi));
                 return;
             }
 #pragma unroll
-            for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase16<COST>(P, raw[i], tlo, thi));
+            for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase16<COST, R>(P, raw[i], tlo, thi));
         };
         // ---- round 0 (PAT8)
         if (PH == 1) phase_all();
-        bfly16<MIX, MA, PAT8>(v, P.A, round_mask<K, SEQ>(P.maskA, 0));
+        bfly16<MIX, MA, PAT8, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 0));
         if constexpr (SEQ == SEQ_840) {
-            if (HAS_B) bfly16<MIX, MB, PAT8>(v, P.B, round_mask<K, SEQ>(P.maskB, 0));
+            if (HAS_B) bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 0));
             transpose<PAT8, PAT0>(tile, v, tid);
-            bfly16<MIX, MA, PAT0>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
-            if (HAS_B) bfly16<MIX, MB, PAT0>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
+            bfly16<MIX, MA, PAT0, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+            if (HAS_B) bfly16<MIX, MB, PAT0, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
             transpose<PAT0, PAT4>(tile, v, tid);
-            bfly16<MIX, MA, PAT4>(v, P.A, round_mask<K, SEQ>(P.maskA, 2));
-            if (HAS_B) bfly16<MIX, MB, PAT4>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
+            bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 2));
+            if (HAS_B) bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
         } else if constexpr (SEQ == SEQ_84) {
-            if (HAS_B) bfly16<MIX, MB, PAT8>(v, P.B, round_mask<K, SEQ>(P.maskB, 0));
+            if (HAS_B) bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 0));
             transpose<PAT8, PAT4>(tile, v, tid);
-            bfly16<MIX, MA, PAT4>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
-            if (HAS_B) bfly16<MIX, MB, PAT4>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
+            bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+            if (HAS_B) bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
         } else if constexpr (SEQ == SEQ_84048) {
             transpose<PAT8, PAT0>(tile, v, tid);
-            bfly16<MIX, MA, PAT0>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+            bfly16<MIX, MA, PAT0, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
             transpose<PAT0, PAT4>(tile, v, tid);
-            bfly16<MIX, MA, PAT4>(v, P.A, round_mask<K, SEQ>(P.maskA, 2));
+            bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 2));
             phase_all();
-            bfly16<MIX, MB, PAT4>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
+            bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
             transpose<PAT4, PAT0>(tile, v, tid);
-            bfly16<MIX, MB, PAT0>(v, P.B, round_mask<K, SEQ>(P.maskB, 3));
+            bfly16<MIX, MB, PAT0, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 3));
             transpose<PAT0, PAT8>(tile, v, tid);
-            bfly16<MIX, MB, PAT8>(v, P.B, round_mask<K, SEQ>(P.maskB, 4));
+            bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 4));
         } else {  // SEQ_848
             transpose<PAT8, PAT4>(tile, v, tid);
-            bfly16<MIX, MA, PAT4>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+            bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
             phase_all();
-            bfly16<MIX, MB, PAT4>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
+            bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
             transpose<PAT4, PAT8>(tile, v, tid);
-            bfly16<MIX, MB, PAT8>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
+            bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
         }
         // ---- store (+ expectation) in the last round's pattern
-        const double fs = P.final_scale;
+        const R fs = (R)P.final_scale;
         if (PH != 3 && P.expect) {  // cost entries of the last pattern (final pass with a phase)
             const char *cl = cs + thrL * CB;
 #pragma unroll
             for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i]);
         }
-        char *psl = reinterpret_cast<char *>(P.psi + base + thrL);
+        char *psl = reinterpret_cast<char *>(static_cast<T *>(P.psi) + base + thrL);
 #pragma unroll
         for (int i = 0; i < kRegs; ++i) {
-            double2 x = v[i];
-            if (MIX == MIX_RX) x = make_double2(x.x * fs, x.y * fs);
-            if (P.expect) eacc += decode_cost<COST>(P, raw[i]) * (x.x * x.x + x.y * x.y);
-            st_stream(reinterpret_cast<double2 *>(psl + P.roff[LAST][i]), x);
+            T x = v[i];
+            if (MIX == MIX_RX) x = Cx<R>::make(x.x * fs, x.y * fs);
+            if (P.expect) eacc += decode_cost<COST>(P, raw[i]) * ((double)x.x * x.x + (double)x.y * x.y);
+            st_stream(reinterpret_cast<T *>(psl + P.roff[LAST][i]), x);
         }
     }
     if (P.expect) {
@@ -496,17 +523,18 @@ struct PassMaps {
     alignas(64) CUtensorMap cost;
 };
 
-template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K>
+template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R = double>
 static int launch_pass16(const PassParams &P, const PassMaps &M, int grid, cudaStream_t st) {
     static bool configured = false;
-    const size_t smem = (size_t)(kTilePadded + (kTableLo + kMaxTableHi) * kCopies) * sizeof(double2);
+    constexpr int CP = table_copies<R>();
+    const size_t smem = (size_t)(kTilePadded + (kTableLo + kMaxTableHi) * CP) * sizeof(C2<R>);
     if (!configured) {
-        cudaFuncSetAttribute(k_pass16<MIX, COST, SEQ, PH, MA, MB, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_pass16<MIX, COST, SEQ, PH, MA, MB, K, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         configured = true;
     }
-    const size_t need = (size_t)(kTilePadded + (kTableLo + P.table_hi) * kCopies) * sizeof(double2);
-    k_pass16<MIX, COST, SEQ, PH, MA, MB, K><<<grid, kThreads, need, st>>>(P, M.state, M.cost);
+    const size_t need = (size_t)(kTilePadded + (kTableLo + P.table_hi) * CP) * sizeof(C2<R>);
+    k_pass16<MIX, COST, SEQ, PH, MA, MB, K, R><<<grid, kThreads, need, st>>>(P, M.state, M.cost);
     FQ_LAUNCHED("k_pass16");
     return FQ_OK;
 }
@@ -515,18 +543,18 @@ static int launch_pass16(const PassParams &P, const PassMaps &M, int grid, cudaS
 // ph/ma/mb/k as the k_pass16 parameters (ma/mb already normalised by the
 // caller); a mask class k without an instantiation runs with the run-time
 // masks (K_RUNTIME), which PassParams always carries.
-template <int MIX, int COST, int SEQ>
+template <int MIX, int COST, int SEQ, typename R = double>
 static int select_seq(const PassParams &P, const PassMaps &M, int ph, int ma, int mb, int k, int grid, cudaStream_t st) {
     constexpr bool kHigh = SEQ == SEQ_84 || SEQ == SEQ_848;
 #define FQ_K(PHV, MAV, MBV)                                                                                  \
     if (ph == PHV && ma == MAV && mb == MBV) {                                                               \
-        if (k == K_FULL) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_FULL>(P, M, grid, st);          \
+        if (k == K_FULL) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_FULL, R>(P, M, grid, st);          \
         if constexpr (kHigh && MIX == MIX_RX) {                                                              \
-            if (k == 1) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 1>(P, M, grid, st);                \
-            if (k == 2) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 2>(P, M, grid, st);                \
-            if (k == 3) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 3>(P, M, grid, st);                \
+            if (k == 1) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 1, R>(P, M, grid, st);                \
+            if (k == 2) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 2, R>(P, M, grid, st);                \
+            if (k == 3) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 3, R>(P, M, grid, st);                \
         }                                                                                                    \
-        return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_RUNTIME>(P, M, grid, st);                        \
+        return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_RUNTIME, R>(P, M, grid, st);                        \
     }
     if constexpr (seq_heavy(SEQ)) {
         if constexpr (MIX == MIX_RX) {
@@ -549,5 +577,11 @@ int launch_pass_rx_u16_heavy(const PassParams &P, const PassMaps &M, int seq, in
 int launch_pass_rx_f64_light(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
 int launch_pass_rx_f64_heavy(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
 int launch_pass_su2(const PassParams &P, const PassMaps &M, int cost, int seq, int ph, int mb, int k, int grid, cudaStream_t st);
+// complex64 states (R = float): X mixer, all round programs, one unit per cost encoding
+int launch_pass_c64_u16(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
+int launch_pass_c64_f64(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
+// complex64 states (R = float): X mixer, all round programs, one unit per cost encoding
+int launch_pass_c64_u16(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
+int launch_pass_c64_f64(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
 
 }  // namespace fq

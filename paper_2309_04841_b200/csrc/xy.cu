@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__
     __shared__ double red[kThreads / 32];
     const int tid = threadIdx.x;
     if (COST == FQ_COST_U16 && PH) {
-        if (P.table_hi > 0) build_phase_tables(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
+        if (P.table_hi > 0) build_phase_tables<double>(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
         __syncthreads();
     }
     const long long thr_first = xy_tphys(P, P.rounds[0], tid);

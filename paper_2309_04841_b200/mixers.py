@@ -21,6 +21,7 @@ from dataclasses import dataclass
 from typing import Callable, Sequence
 
 import numpy as np
+import torch
 
 from . import _lib
 from .statevec import _OnDevice, num_qubits
@@ -106,6 +107,7 @@ def run_program(psi, n: int, mixer: str, layers: Sequence[tuple], dc=None, su2: 
     desc.init_amp = init_amp
     desc.expectation_dev = expectation_out.data_ptr() if expectation_out is not None else None
     desc.scratch = _lib.scratch().data_ptr()
+    desc.state_kind = _lib.STATE_C64 if psi.dtype == torch.complex64 else _lib.STATE_C128
     _lib.check(_lib.load().fq_qaoa_evolve(ctypes.byref(desc), _lib.stream()), "fq_qaoa_evolve")
 
 

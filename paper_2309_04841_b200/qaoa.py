@@ -88,22 +88,23 @@ _COST_MEMO: "OrderedDict[TermPolynomial, DeviceCosts]" = OrderedDict()
 _MEMO_SIZE = 32
 
 
-def _device_costs_for(poly: TermPolynomial) -> DeviceCosts:
-    """Diagonal of a polynomial sized for one state of the same n next to it:
-    float64 + uint16 levels when 26 B/amplitude fit, else (integer / dyadic
-    weights, e.g. LABS n = 33 on one B200) the uint16 levels alone, computed
-    exactly from the terms — the reference's n <= 30 cap (terms.py:109-113)
-    becomes this device-memory check."""
+def _device_costs_for(poly: TermPolynomial, state_bytes: int = 16) -> DeviceCosts:
+    """Diagonal of a polynomial sized for one state of the same n next to it
+    (``state_bytes`` per amplitude: 16 complex128, 8 complex64): float64 +
+    uint16 levels when they fit, else (integer / dyadic weights, e.g. LABS
+    n = 33 complex128 or n = 34 complex64 on one B200) the uint16 levels
+    alone, computed exactly from the terms — the reference's n <= 30 cap
+    (terms.py:109-113) becomes this device-memory check."""
     free, _ = torch.cuda.mem_get_info(_lib.device())
     size = 1 << poly.n
-    if size * (16 + 8 + 2) <= 0.95 * free:
+    if size * (state_bytes + 8 + 2) <= 0.95 * free:
         return DeviceCosts.from_polynomial(poly)
-    if size * (16 + 2) <= 0.95 * free:
+    if size * (state_bytes + 2) <= 0.95 * free:
         try:
             return DeviceCosts.from_polynomial(poly, keep_f64=False)
         except MemoryError:
             pass
-    _check_fits(poly.n, 16 + 8, "state vector + cost vector")
+    _check_fits(poly.n, state_bytes + 8, "state vector + cost vector")
     return DeviceCosts.from_polynomial(poly)
 
 
@@ -133,7 +134,23 @@ def resolve_costs(problem) -> tuple[DeviceCosts, int]:
     return dc, dc.n
 
 
-def _initial_state(n: int, mixer: Mixer, initial, out: torch.Tensor | None = None) -> tuple[torch.Tensor, bool]:
+def state_dtype(dtype) -> torch.dtype:
+    """complex128 (the reference's state, default) or complex64 (optional
+    single-precision state: X mixer only; 1e-4 tolerance)."""
+    if dtype is None:
+        return torch.complex128
+    if dtype in (torch.complex128, torch.complex64):
+        return dtype
+    name = np.dtype(dtype).name if not isinstance(dtype, str) else dtype
+    if name in ("complex128", "c16", "complex"):
+        return torch.complex128
+    if name in ("complex64", "c8"):
+        return torch.complex64
+    raise ValueError(f"unsupported state dtype {dtype!r} (complex128 or complex64)")
+
+
+def _initial_state(n: int, mixer: Mixer, initial, out: torch.Tensor | None = None,
+                   dtype: torch.dtype = torch.complex128) -> tuple[torch.Tensor, bool]:
     """(device state, generate-|+>-in-kernel flag) — reference qaoa.py:90-103.
     ``out``: caller-owned buffer the |+> program evolves into (no allocation)."""
     dev = _lib.device()
@@ -141,11 +158,11 @@ def _initial_state(n: int, mixer: Mixer, initial, out: torch.Tensor | None = Non
         if isinstance(initial, torch.Tensor):
             if initial.numel() != 1 << n:
                 raise ValueError(f"initial state has {initial.numel()} amplitudes, expected {1 << n}")
-            return initial.to(device=dev, dtype=torch.complex128).clone().contiguous(), False
+            return initial.to(device=dev, dtype=dtype).clone().contiguous(), False
         arr = np.array(initial, dtype=np.complex128)
         if arr.size != 1 << n:
             raise ValueError(f"initial state has {arr.size} amplitudes, expected {1 << n}")
-        return torch.from_numpy(arr.reshape(-1)).to(dev), False
+        return torch.from_numpy(arr.reshape(-1)).to(dev).to(dtype), False
     if mixer.preserves_hamming_weight:
         raise ValueError(
             "XY mixers act within a fixed-popcount sector; pass an initial "
@@ -154,15 +171,22 @@ def _initial_state(n: int, mixer: Mixer, initial, out: torch.Tensor | None = Non
     if out is not None:
         return out, True
     try:
-        return torch.empty(1 << n, dtype=torch.complex128, device=dev), True
+        return torch.empty(1 << n, dtype=dtype, device=dev), True
     except torch.OutOfMemoryError as exc:
         raise MemoryError(f"state vector for n={n} does not fit in device memory "
                           f"(shard it: simulate_qaoa_distributed / ShardedQaoaSimulator)") from exc
 
 
 def _evolve(dc: DeviceCosts, n: int, mixer: Mixer, params: QaoaParams, initial,
-            out: torch.Tensor | None = None) -> QaoaResult:
-    state, init = _initial_state(n, mixer, initial, out=out)
+            out: torch.Tensor | None = None, dtype: torch.dtype = torch.complex128) -> QaoaResult:
+    if dtype == torch.complex64:
+        if mixer.kind != "x":
+            raise ValueError(f"complex64 states run the X mixer only (got {mixer.kind!r}); use complex128")
+        if n <= 12:
+            # on-chip sizes: the resident fp64 program, rounded to complex64 once at the end
+            res = _evolve(dc, n, mixer, params, initial)
+            return QaoaResult(res.state_device.to(torch.complex64), dc, res._expectation_dev)
+    state, init = _initial_state(n, mixer, initial, out=out, dtype=dtype)
     layers = [(g, b, 1, 0, n) for g, b in zip(params.gammas, params.betas)]
     exp_dev = torch.empty(1, dtype=torch.float64, device=state.device)
     run_program(state, n, mixer.kind, layers, dc=dc, su2=mixer.su2_table(params.betas, n),
@@ -174,16 +198,21 @@ class QaoaSimulator:
     """Simulator bound to one problem; the cost diagonal is computed once, on
     the GPU, at construction (reference qaoa.py:106-166)."""
 
-    def __init__(self, n: int | None = None, *, terms=None, costs=None, mixer: "str | Mixer" = "x") -> None:
+    def __init__(self, n: int | None = None, *, terms=None, costs=None, mixer: "str | Mixer" = "x",
+                 dtype=None) -> None:
+        """``dtype``: state type, complex128 (default, the reference's) or
+        complex64 (optional: half the HBM traffic and memory, X mixer only,
+        amplitudes / objective within 1e-4 of complex128)."""
         if (terms is None) == (costs is None):
             raise ValueError("pass exactly one of terms= or costs=")
+        self.dtype = state_dtype(dtype)
         if terms is not None:
             if not isinstance(terms, TermPolynomial):
                 if n is None:
                     raise ValueError("a plain term list needs n")
                 terms = TermPolynomial.from_pairs(n, terms)
             _check_fits(terms.n, 2, "cost vector")
-            self._dc = _device_costs_for(terms)
+            self._dc = _device_costs_for(terms, state_bytes=16 if self.dtype == torch.complex128 else 8)
             instrumentation.bump("precompute")
             self.n = terms.n
         else:
@@ -192,6 +221,8 @@ class QaoaSimulator:
         if n is not None and n != self.n:
             raise ValueError(f"n={n} disagrees with problem size {self.n}")
         self.mixer = Mixer.parse(mixer)
+        if self.dtype == torch.complex64 and self.mixer.kind != "x":
+            raise ValueError(f"complex64 states run the X mixer only (got {self.mixer.kind!r})")
         self._buffer: torch.Tensor | None = None
 
     @property
@@ -212,9 +243,9 @@ class QaoaSimulator:
         out = None
         if reuse_buffer:
             if self._buffer is None:
-                self._buffer = torch.empty(1 << self.n, dtype=torch.complex128, device=_lib.device())
+                self._buffer = torch.empty(1 << self.n, dtype=self.dtype, device=_lib.device())
             out = self._buffer
-        return _evolve(self._dc, self.n, self.mixer, params, initial, out=out)
+        return _evolve(self._dc, self.n, self.mixer, params, initial, out=out, dtype=self.dtype)
 
     def simulate_qaoa_batched(self, gammas, betas) -> np.ndarray:
         """Expectations of many parameter sets at once (n <= 12: each set
@@ -223,7 +254,7 @@ class QaoaSimulator:
         b = np.ascontiguousarray(betas, dtype=np.float64)
         if g.ndim != 2 or g.shape != b.shape:
             raise ValueError("gammas and betas must both be [batch, p]")
-        if self.n > 12 or self.mixer.kind == "custom":
+        if self.n > 12 or self.mixer.kind == "custom" or self.dtype == torch.complex64:
             return np.array([self.get_expectation(self.simulate_qaoa(gg, bb)) for gg, bb in zip(g, b)])
         if self.mixer.preserves_hamming_weight:
             raise ValueError("XY mixers need an explicit initial state; use simulate_qaoa")
@@ -244,7 +275,8 @@ class QaoaSimulator:
     def get_probabilities(self, result: QaoaResult, preserve_state: bool = True) -> np.ndarray:
         psi = result.state_device
         work = psi.clone() if preserve_state else psi
-        _lib.call("fq_abs2_inplace", work.data_ptr(), work.numel(), _lib.stream())
+        fn = "fq_abs2_inplace_c64" if work.dtype == torch.complex64 else "fq_abs2_inplace"
+        _lib.call(fn, work.data_ptr(), work.numel(), _lib.stream())
         if not preserve_state:
             result._mutated()
         return torch.view_as_real(work)[:, 0].cpu().numpy()
@@ -274,18 +306,19 @@ class QaoaSimulator:
         return min(max(total, 0.0), 1.0)
 
 
-def simulate_qaoa(problem, params: QaoaParams, mixer: "str | Mixer" = "x", initial=None) -> QaoaResult:
+def simulate_qaoa(problem, params: QaoaParams, mixer: "str | Mixer" = "x", initial=None,
+                  dtype=None) -> QaoaResult:
     """One-shot evolution; the device diagonal is memoised per polynomial
-    (reference qaoa.py:169-182)."""
+    (reference qaoa.py:169-182).  ``dtype``: see QaoaSimulator."""
     dc, n = resolve_costs(problem)
-    return _evolve(dc, n, Mixer.parse(mixer), params, initial)
+    return _evolve(dc, n, Mixer.parse(mixer), params, initial, dtype=state_dtype(dtype))
 
 
-def qaoa_objective(problem, params: QaoaParams, mixer: "str | Mixer" = "x", initial=None) -> float:
+def qaoa_objective(problem, params: QaoaParams, mixer: "str | Mixer" = "x", initial=None, dtype=None) -> float:
     """Expected cost of the evolved state (reference qaoa.py:185-194)."""
-    result = simulate_qaoa(problem, params, mixer=mixer, initial=initial)
+    result = simulate_qaoa(problem, params, mixer=mixer, initial=initial, dtype=dtype)
     return float(result._expectation_dev.item())
 
 
 __all__ = ["QaoaParams", "QaoaResult", "QaoaSimulator", "simulate_qaoa", "qaoa_objective", "resolve_costs",
-           "num_qubits"]
+           "num_qubits", "state_dtype"]

@@ -157,7 +157,8 @@ def expectation_device(psi: torch.Tensor, dc) -> torch.Tensor:
     """sum_k c_k |psi_k|^2 into a 1-element device tensor (no host sync)."""
     out = torch.empty(1, dtype=torch.float64, device=psi.device)
     kind, cp, scale, offset = dc.kernel_view()
-    _lib.call("fq_expectation", psi.data_ptr(), cp, kind, scale, offset, psi.numel(), out.data_ptr(),
+    fn = "fq_expectation_c64" if psi.dtype == torch.complex64 else "fq_expectation"
+    _lib.call(fn, psi.data_ptr(), cp, kind, scale, offset, psi.numel(), out.data_ptr(),
               _lib.scratch().data_ptr(), _lib.stream())
     return out
 
@@ -175,7 +176,8 @@ def expectation(state, costs) -> float:
 def overlap_device(psi: torch.Tensor, dc, cutoff: float) -> torch.Tensor:
     out = torch.empty(1, dtype=torch.float64, device=psi.device)
     kind, cp, scale, offset = dc.kernel_view()
-    _lib.call("fq_masked_probability", psi.data_ptr(), cp, kind, scale, offset, psi.numel(), float(cutoff),
+    fn = "fq_masked_probability_c64" if psi.dtype == torch.complex64 else "fq_masked_probability"
+    _lib.call(fn, psi.data_ptr(), cp, kind, scale, offset, psi.numel(), float(cutoff),
               out.data_ptr(), _lib.scratch().data_ptr(), _lib.stream())
     return out
 

@@ -1,0 +1,141 @@
+"""complex64 states (north star: "complex128, with complex64 optional", fp32
+tolerance 1e-4): the single-precision pass program against the fp64 CPU
+oracle on the same inputs, the observables on complex64 states, the
+full-size headline configuration against the reference's own fingerprints,
+and the documented limits (X mixer only)."""
+
+import numpy as np
+import pytest
+import torch
+
+from _helpers import random_pairs
+from _large import CASES
+from oracle import oracle as O
+from paper_2309_04841_b200 import QaoaParams, QaoaSimulator, TermPolynomial, qaoa_objective, simulate_qaoa
+from paper_2309_04841_b200 import _lib, statevec
+from paper_2309_04841_b200.problems import labs_terms
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4  # north star: fp32 results within 1e-4 relative
+
+
+def _check_state(got, ref):
+    assert got.dtype == np.complex64
+    err = np.linalg.norm(got.astype(np.complex128) - ref) / np.linalg.norm(ref)
+    assert err <= TOL, err
+    np.testing.assert_allclose(got, ref, rtol=0, atol=TOL * np.abs(ref).max())
+
+
+def _check_energy(E, e_ref, costs):
+    assert abs(E - e_ref) <= TOL * max(abs(e_ref), np.abs(costs).max()), (E, e_ref)
+
+
+@pytest.mark.parametrize("n,p,seed", [(13, 1, 0), (14, 3, 1), (16, 4, 2), (19, 2, 3), (22, 3, 4), (24, 2, 5)])
+def test_c64_labs_vs_oracle(n, p, seed):
+    """uint16 levels + fp32 phase tables, every round program of the plan."""
+    rng = np.random.default_rng(seed)
+    g, b = rng.uniform(-1, 1, p), rng.uniform(-1.6, 1.6, p)
+    sim = QaoaSimulator(terms=labs_terms(n), dtype=torch.complex64)
+    assert sim.device_costs.u16 is not None
+    res = sim.simulate_qaoa(g, b)
+    assert res.state_device.dtype == torch.complex64
+    costs = sim.get_cost_diagonal()
+    ref = O.simulate(costs, g, b)
+    _check_state(sim.get_statevector(res), ref)
+    e_ref = O.expectation(ref, costs)
+    _check_energy(sim.get_expectation(res), e_ref, costs)           # fused into the last pass
+    _check_energy(sim.get_expectation(res, costs=costs), e_ref, costs)  # standalone c64 reduction
+
+
+@pytest.mark.parametrize("n,p,seed", [(13, 2, 10), (17, 3, 11)])
+def test_c64_float_costs_vs_oracle(n, p, seed):
+    """Float-weight diagonal: float64 costs, angle reduced in fp64, sincos per amplitude."""
+    rng = np.random.default_rng(seed)
+    poly = TermPolynomial.from_pairs(n, random_pairs(rng, n, max_terms=3 * n))
+    g, b = rng.uniform(-1, 1, p), rng.uniform(-1, 1, p)
+    sim = QaoaSimulator(terms=poly, dtype="complex64")
+    assert sim.device_costs.u16 is None
+    res = sim.simulate_qaoa(g, b)
+    costs = sim.get_cost_diagonal()
+    ref = O.simulate(costs, g, b)
+    _check_state(sim.get_statevector(res), ref)
+    _check_energy(sim.get_expectation(res), O.expectation(ref, costs), costs)
+
+
+def test_c64_observables_and_special_layers():
+    """gamma = 0 layers, beta = pi/2 (the (cot, 1) butterfly form), an explicit
+    initial state, probabilities and the overlap on a complex64 state."""
+    n = 15
+    poly = labs_terms(n)
+    sim = QaoaSimulator(terms=poly, dtype=np.complex64)
+    rng = np.random.default_rng(3)
+    init = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    init /= np.linalg.norm(init)
+    g = [0.0, 0.3, 0.0, 0.2]
+    b = [np.pi / 2, 0.3, 1.2, -2.0]
+    res = sim.simulate_qaoa(g, b, initial=init)
+    costs = sim.get_cost_diagonal()
+    ref = O.simulate(costs, g, b, "x", init)
+    _check_state(res.state, ref)
+    probs = sim.get_probabilities(res)
+    assert probs.dtype == np.float32
+    np.testing.assert_allclose(probs, np.abs(ref) ** 2, rtol=0, atol=TOL * (np.abs(ref) ** 2).max())
+    assert sim.get_overlap(res) == pytest.approx(O.overlap(ref, costs), abs=TOL)
+    assert statevec.overlap_device(res.state_device, sim.device_costs, costs.min()).item() == pytest.approx(
+        O.overlap(ref, costs), abs=TOL)
+
+
+def test_c64_small_n_and_module_functions():
+    """n <= 12 runs the resident fp64 program and rounds once; the module-level
+    simulate_qaoa / qaoa_objective take the same dtype."""
+    for n in (6, 12, 13):
+        poly = labs_terms(n)
+        params = QaoaParams((0.2, -0.4), (0.7, 0.3))
+        res = simulate_qaoa(poly, params, dtype="complex64")
+        assert res.state.dtype == np.complex64
+        costs = res.costs
+        ref = O.simulate(costs, params.gammas, params.betas)
+        _check_state(res.state, ref)
+        _check_energy(qaoa_objective(poly, params, dtype="complex64"), O.expectation(ref, costs), costs)
+
+
+def test_c64_limits():
+    with pytest.raises(ValueError):
+        QaoaSimulator(terms=labs_terms(14), mixer="xy-ring", dtype="complex64")
+    with pytest.raises(ValueError):
+        QaoaSimulator(terms=labs_terms(14), dtype="float32")
+    # the ABI refuses what the kernels do not implement, loudly
+    from paper_2309_04841_b200.mixers import run_program
+
+    psi = torch.empty(1 << 14, dtype=torch.complex64, device=_lib.device())
+    with pytest.raises(RuntimeError):
+        run_program(psi, 14, "xy-ring", [(0.0, 0.3, 0, 0, 14)])
+
+
+def test_c64_reuse_buffer_and_determinism():
+    sim = QaoaSimulator(terms=labs_terms(18), dtype="complex64")
+    g, b = [0.1, 0.2, 0.3], [0.5, 0.4, 0.3]
+    vals = {sim.get_expectation(sim.simulate_qaoa(g, b, reuse_buffer=True)) for _ in range(3)}
+    assert len(vals) == 1
+    assert sim._buffer.dtype == torch.complex64
+
+
+def test_c64_headline_config_vs_reference_fingerprint(golden_large):
+    """LABS n = 26 p = 10 (the headline workload) in complex64 against the
+    reference's own complex128 outputs: objective, overlap, 4096 sampled
+    amplitudes and the 1024 block norms, all at the fp32 tolerance."""
+    name = "labs26_x_p10"
+    make, kind, _ = CASES[name]
+    sim = QaoaSimulator(terms=make(), dtype="complex64")
+    res = sim.simulate_qaoa(golden_large[f"{name}/gammas"], golden_large[f"{name}/betas"])
+    E = sim.get_expectation(res)
+    e_ref = float(golden_large[f"{name}/E"])
+    assert abs(E - e_ref) <= TOL * abs(e_ref), (E, e_ref)
+    assert sim.get_overlap(res) == pytest.approx(float(golden_large[f"{name}/overlap"]), abs=TOL)
+    state = sim.get_statevector(res)
+    amp = golden_large[f"{name}/amp"]
+    np.testing.assert_allclose(state[golden_large[f"{name}/idx"]], amp, rtol=0, atol=TOL * np.abs(amp).max())
+    blocks = (np.abs(state.astype(np.complex128)) ** 2).reshape(1024, -1).sum(axis=1)
+    ref_blocks = golden_large[f"{name}/block_norm2"]
+    np.testing.assert_allclose(blocks, ref_blocks, rtol=TOL, atol=0)
