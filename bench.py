@@ -287,7 +287,8 @@ def main():
 
     # ------------------------------------------------------------ byte model of the step (per GPU)
     lay = (_lib.FqLayer * p)(*[_lib.FqLayer(*lt) for lt in layers])
-    passes = _lib.load().fq_plan_x_passes(n_local, p, lay)
+    skind = _lib.STATE_C64 if c64 else _lib.STATE_C128
+    passes = _lib.load().fq_plan_x_passes(n_local, p, lay, skind)
     n_phase = sum(1 for gi in g if gi != 0.0)
     P_survey = -(-n_local // 12)
     survey_bytes = p * (P_survey * 2 * S + Cb) + (S + Cb)
@@ -297,7 +298,7 @@ def main():
     else:
         post = p * (1 if k > 0 else 0)  # the k-position pass after each exchange
         local_passes = passes * p if False else None
-        per_layer = _lib.load().fq_plan_x_passes(n_local, 1, lay)
+        per_layer = _lib.load().fq_plan_x_passes(n_local, 1, lay, skind)
         tile_bytes = p * per_layer * 2 * S - S + n_phase * Cb + post * 2 * S + S + Cb
         launches = p * (per_layer + (1 if k > 0 else 0)) + 2
         del local_passes

@@ -150,6 +150,12 @@ int fq_masked_probability_c64(const void *psi, const void *costs, int cost_kind,
                               double offset, int64_t size, double cutoff, double *out_dev,
                               double *scratch, void *stream);
 
+/* levels[k] -= delta for every k (all levels >= delta): moves the level
+ * origin to the diagonal's minimum after packing from a bound (decode offset
+ * grows by delta*scale, exactly), so the phase tables cover the levels in use.
+ * levels 16-B aligned. */
+int fq_rebase_u16(uint16_t *levels, int64_t size, int delta, void *stream);
+
 /* Lossless uint16 packing of a float64 diagonal (terms.py:155-175):
  * out[k] = rint((c_k - offset)/scale); *bad_dev set nonzero if any level > 65535 or
  * scale*v + offset != c_k bit-for-bit. */
@@ -209,9 +215,10 @@ int fq_qaoa_evolve_batched(int n, int mixer, const void *costs, int cost_kind, d
                            const double *betas, const void *psi_init, void *psi_out,
                            double *out_dev, void *stream);
 
-/* Number of HBM passes fq_qaoa_evolve will run for an X-mixer program (for the
- * byte model in bench.py / DESIGN.md). */
-int fq_plan_x_passes(int n, int n_layers, const fq_layer *layers);
+/* Number of HBM passes fq_qaoa_evolve will run for an X-mixer program on a
+ * state of state_kind (FQ_STATE_*; the plan depends on the bytes per
+ * amplitude), for the byte model in bench.py / DESIGN.md. */
+int fq_plan_x_passes(int n, int n_layers, const fq_layer *layers, int state_kind);
 
 /* ------------------------------------------------------------------ *
  * Sharded state over peer memory                                       *

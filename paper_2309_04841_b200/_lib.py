@@ -59,9 +59,10 @@ _SIGS = {
     "fq_cost_minmax": ([P, I, D, D, I64, P, P, P], I),
     "fq_masked_probability": ([P, P, I, D, D, I64, D, P, P, P], I),
     "fq_compact_u16": ([P, P, I64, D, D, P, P], I),
+    "fq_rebase_u16": ([P, I64, I, P], I),
     "fq_qaoa_evolve": ([ctypes.POINTER(FqEvolveDesc), P], I),
     "fq_qaoa_evolve_batched": ([I, I, P, I, D, D, I, I, P, P, P, P, P, P], I),
-    "fq_plan_x_passes": ([I, I, ctypes.POINTER(FqLayer)], I),
+    "fq_plan_x_passes": ([I, I, ctypes.POINTER(FqLayer), I], I),
     "fq_set_option": ([ctypes.c_char_p, I], I),
     "fq_last_passes": ([P, P, I], I),
     "fq_plan_xy_passes": ([I, I, P], I),

@@ -121,9 +121,16 @@ class DeviceCosts:
         if int(bad.item()) != 0:
             return False
         self.u16 = out
-        self.levels = 2 * ta.abs_sum + 1
         self.scale = 2.0 ** -ta.shift
         self.offset = float(lo) * self.scale
+        # the levels were packed from the bound -sum|w|: move the origin to the
+        # observed minimum (exact: dyadic values) so the phase tables (levels <
+        # 16384) cover the range in use, e.g. LABS n = 34 (2 sum|w| + 1 > 16384)
+        c_lo, c_hi = self.minmax()
+        delta = int(round((c_lo - self.offset) / self.scale))
+        _lib.call("fq_rebase_u16", out.data_ptr(), size, delta, _lib.stream())
+        self.offset += delta * self.scale
+        self.levels = int(round((c_hi - c_lo) / self.scale)) + 1
         return True
 
     # -------------------------------------------------------------- views

@@ -233,21 +233,26 @@ static std::vector<std::vector<int>> split_even(const std::vector<int> &v, int p
 }
 
 // Candidate orderings of the target groups of one layer (the first and last
-// group of a layer are the fusion points with the neighbouring layers):
-//   0: [low, high chunks of <= 10]              (all-qubit passes, legacy)
-//   1: [high_0, low, high_1 .. high_m-1], high chunks of <= 8 targets, so both
-//      fusion points are small groups (3-round fused passes)
-static std::vector<std::vector<int>> candidate_groups(const std::vector<int> &targets, int cand) {
+// group of a layer are the fusion points with the neighbouring layers), high
+// targets in even chunks of <= tmax:
+//   style 0: [low, high chunks]                 (all-qubit passes, legacy)
+//   style 1: [high_0, low, high_1 .. high_m-1], so both fusion points are
+//      small groups (3-round fused passes)
+// A chunk of t high targets leaves 12 - t low spectators: the tile's global
+// accesses are runs of 2^(12-t) amplitudes, which sets the pass's bandwidth
+// (run_factor), so fewer targets per pass can win at large n.
+static std::vector<std::vector<int>> candidate_groups(const std::vector<int> &targets, int style, int tmax) {
     std::vector<int> low, high;
     for (int q : targets) (q < kTileBits ? low : high).push_back(q);
     std::vector<std::vector<int>> out;
-    if (cand == 0 || high.empty() || low.empty()) {
+    const int chunks = (int)((high.size() + tmax - 1) / tmax);
+    if (style == 0 || high.empty() || low.empty()) {
         if (!low.empty()) out.push_back(low);
         if (!high.empty())
-            for (auto &c : split_even(high, (int)((high.size() + 9) / 10))) out.push_back(c);
+            for (auto &c : split_even(high, chunks)) out.push_back(c);
         return out;
     }
-    auto hs = split_even(high, (int)((high.size() + 7) / 8));
+    auto hs = split_even(high, chunks);
     out.push_back(hs[0]);
     out.push_back(low);
     for (size_t i = 1; i < hs.size(); ++i) out.push_back(hs[i]);
@@ -278,9 +283,9 @@ static void rx_coef(double beta, CoefSet &C, double &f) {
 }
 
 static int g_fuse = 1;
-static int g_prefetch = 1;   // L2 prefetch distance (grid strides)
+static int g_prefetch = -1;  // L2 prefetch distance (grid strides); -1: 1 for runs >= 256 B, else 0
 static int g_phase_tables = 1;
-static int g_plan = -1;      // -1: choose by cost model, else force candidate
+static int g_plan = -1;      // -1: choose by cost model, else force style (0 / 1, legacy chunk sizes)
 static int g_time_passes = 0;
 static int g_probe = 0;      // development probe bits (PassParams::probe)
 static int g_zigzag = 1;     // alternate the tile walk direction pass to pass (L2 reuse across passes)  // record a CUDA event after every pass of the next programs
@@ -292,8 +297,8 @@ struct PassRecord {
 static std::vector<PassRecord> g_last_plan;
 static std::vector<cudaEvent_t> g_events;  // g_last_plan.size() + 1 when timing is on
 
-static std::vector<PlannedPass> plan_with(int n, int nl, const fq_layer *layers, std::vector<Group> &groups, int cand,
-                                          bool fuse) {
+static std::vector<PlannedPass> plan_with(int n, int nl, const fq_layer *layers, std::vector<Group> &groups, int style,
+                                          int tmax, bool fuse) {
     groups.clear();
     std::vector<PlannedPass> seq;
     std::vector<int> prev_targets;
@@ -307,7 +312,7 @@ static std::vector<PlannedPass> plan_with(int n, int nl, const fq_layer *layers,
             ng = prev_ng;
         } else {
             gbase = (int)groups.size();
-            auto chunks = candidate_groups(targets, cand);
+            auto chunks = candidate_groups(targets, style, tmax);
             for (auto &c : chunks) groups.push_back(make_group(n, c));
             ng = (int)chunks.size();
             dir = 0;
@@ -362,19 +367,56 @@ static double pass_cost(int seq) {
     }
 }
 
-static std::vector<PlannedPass> plan_x(int n, int nl, const fq_layer *layers, std::vector<Group> &groups, bool fuse) {
-    if (g_plan >= 0) return plan_with(n, nl, layers, groups, g_plan, fuse);
+// contiguous low tile bits: every global access of the tile is a run of
+// 2^run_bits amplitudes
+static int run_bits_of(const Group &g) {
+    int r = 0;
+    while (r < kTileBits && g.tile_pos[r] == r) ++r;
+    return r;
+}
+
+// Pass time vs the contiguous run length of its accesses, relative to runs
+// >= 512 B (measured on B200, LABS n = 26..34, c128 and c64):
+// heavy (latency-bound, fused) passes lose bandwidth to short runs much faster.
+static double run_factor(long long run_bytes, bool heavy) {
+    if (run_bytes >= 512) return 1.0;
+    if (run_bytes >= 256) return heavy ? 1.13 : 1.04;
+    if (run_bytes >= 128) return heavy ? 2.0 : 1.18;
+    if (run_bytes >= 64) return heavy ? 3.9 : 2.33;
+    return heavy ? 8.0 : 4.7;
+}
+
+static double plan_cost(const std::vector<PlannedPass> &seq, const std::vector<Group> &gs, int n, int elem) {
+    // a state that stays in L2 (126 MB) between passes does not see DRAM run lengths
+    const bool l2_resident = ((long long)elem << n) <= (64LL << 20);
+    double c = 0.0;
+    for (auto &pp : seq) {
+        if (pp.group < 0) {
+            c += 1.0;
+            continue;
+        }
+        const int sq = pass_seq(gs[pp.group], pp);
+        c += pass_cost(sq) * (l2_resident ? 1.0 : run_factor((long long)elem << run_bits_of(gs[pp.group]), seq_heavy(sq)));
+    }
+    return c;
+}
+
+// elem: bytes per amplitude (16 complex128, 8 complex64)
+static std::vector<PlannedPass> plan_x(int n, int nl, const fq_layer *layers, std::vector<Group> &groups, bool fuse,
+                                       int elem) {
+    if (g_plan >= 0) return plan_with(n, nl, layers, groups, g_plan, g_plan == 0 ? 10 : 8, fuse);
     std::vector<PlannedPass> best;
     double best_cost = 1e300;
-    for (int cand = 0; cand < 2; ++cand) {
-        std::vector<Group> gs;
-        auto seq = plan_with(n, nl, layers, gs, cand, fuse);
-        double c = 0.0;
-        for (auto &pp : seq) c += pp.group < 0 ? 1.0 : pass_cost(pass_seq(gs[pp.group], pp));
-        if (c < best_cost - 1e-9) {
-            best_cost = c;
-            best = seq;
-            groups = gs;
+    for (int style = 0; style < 2; ++style) {
+        for (int tmax = 12; tmax >= 4; --tmax) {
+            std::vector<Group> gs;
+            auto seq = plan_with(n, nl, layers, gs, style, tmax, fuse);
+            const double c = plan_cost(seq, gs, n, elem);
+            if (c < best_cost - 1e-9) {
+                best_cost = c;
+                best = seq;
+                groups = gs;
+            }
         }
     }
     return best;
@@ -428,7 +470,9 @@ static int launch_pass(int mix, int cost, bool c64, const PassParams &P, const P
 static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
     const int n = d->n;
     std::vector<Group> groups;
-    auto seq = plan_x(n, d->n_layers, d->layers, groups, g_fuse != 0);
+    const bool c64 = d->state_kind == FQ_STATE_C64;
+    const long long elem = c64 ? (long long)sizeof(float2) : (long long)sizeof(double2);
+    auto seq = plan_x(n, d->n_layers, d->layers, groups, g_fuse != 0, (int)elem);
     const int mix = (d->mixer == FQ_MIXER_X) ? MIX_RX : MIX_SU2;
     const long long n_tiles = 1LL << (n - kTileBits);
     int table_hi = 0;
@@ -437,8 +481,6 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
         table_hi = rows <= kMaxTableHi ? rows : 0;
     }
     bool init_pending = d->init != 0;
-    const bool c64 = d->state_kind == FQ_STATE_C64;
-    const long long elem = c64 ? (long long)sizeof(float2) : (long long)sizeof(double2);
     void *psi = d->psi;
     const long long size = 1LL << n;
     const int sms = sm_count() > 0 ? sm_count() : 148;
@@ -543,7 +585,9 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
         for (int i = 0; i < kTileBits; ++i) P.tile_mask |= 1LL << g.tile_pos[i];
         P.step_dep = deposit(grid, P.tile_mask);
         P.reverse = g_zigzag ? (int)(si & 1) : 0;
-        P.pf_dist = g_prefetch;
+        // the tensor prefetch pays for long runs only: with short runs its many
+        // small requests compete with the demand loads (measured, n = 28..34)
+        P.pf_dist = g_prefetch >= 0 ? g_prefetch : ((elem << run_bits_of(g)) >= 256 ? 1 : 0);
         P.probe = g_probe;
         P.run_bits = 0;
         while (P.run_bits < kTileBits && g.tile_pos[P.run_bits] == P.run_bits) ++P.run_bits;
@@ -751,7 +795,7 @@ int fq_qaoa_evolve(const fq_evolve_desc *d, void *stream) {
 int fq_set_option(const char *name, int value) {
     if (!name) return FQ_ERR_ARG;
     struct { const char *name; int *slot; int lo, hi; } opts[] = {
-        {"prefetch", &g_prefetch, 0, 8},    // L2 prefetch distance of the pass kernel (grid strides)
+        {"prefetch", &g_prefetch, -1, 8},    // L2 prefetch distance of the pass kernel (grid strides)
         {"fuse", &g_fuse, 0, 1},            // fuse the passes at layer boundaries
         {"phase_tables", &g_phase_tables, 0, 1},  // uint16 phase via smem tables (else sincos)
         {"plan", &g_plan, -1, 1},           // group plan: -1 cost model, 0 legacy, 1 small fusion groups
@@ -775,10 +819,10 @@ int fq_set_option(const char *name, int value) {
     return FQ_ERR_ARG;
 }
 
-int fq_plan_x_passes(int n, int n_layers, const fq_layer *layers) {
+int fq_plan_x_passes(int n, int n_layers, const fq_layer *layers, int state_kind) {
     if (n <= kTileBits) return n_layers > 0 ? 1 : 0;
     std::vector<Group> groups;
-    return (int)plan_x(n, n_layers, layers, groups, g_fuse != 0).size();
+    return (int)plan_x(n, n_layers, layers, groups, g_fuse != 0, state_kind == FQ_STATE_C64 ? 8 : 16).size();
 }
 
 int fq_plan_xy_passes(int n, int mixer, int *rounds) {

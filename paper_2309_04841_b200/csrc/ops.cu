@@ -333,6 +333,21 @@ __global__ void k_compact_u16(uint16_t *__restrict__ out, const double *__restri
     }
 }
 
+// levels[k] -= delta, 8 levels per thread-iteration (16-B loads/stores)
+__global__ void k_rebase_u16(uint16_t *__restrict__ lv, int64_t size, unsigned delta) {
+    const int64_t n8 = size >> 3;
+    uint4 *v = reinterpret_cast<uint4 *>(lv);
+    const unsigned d2 = delta | (delta << 16);
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n8; k += (int64_t)gridDim.x * blockDim.x) {
+        uint4 x = v[k];  // lane-wise 16-bit subtraction: every level >= delta, no borrows
+        x.x -= d2, x.y -= d2, x.z -= d2, x.w -= d2;
+        v[k] = x;
+    }
+    for (int64_t k = (n8 << 3) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < size;
+         k += (int64_t)gridDim.x * blockDim.x)
+        lv[k] = (uint16_t)(lv[k] - delta);
+}
+
 }  // namespace fq
 
 using namespace fq;
@@ -562,6 +577,15 @@ int fq_cost_minmax(const void *costs, int cost_kind, double scale, double offset
     if (s) return s;
     k_minmax_final<<<1, 32, 0, S(stream)>>>(scratch, scratch + g, g, out_dev);
     FQ_LAUNCHED("k_minmax_final");
+    return FQ_OK;
+}
+
+int fq_rebase_u16(uint16_t *levels, int64_t size, int delta, void *stream) {
+    FQ_CHECK_ARG(levels && size > 0 && delta >= 0 && delta <= 65535 && (reinterpret_cast<uintptr_t>(levels) & 15) == 0,
+                 "fq_rebase_u16: bad args");
+    if (delta == 0) return FQ_OK;
+    k_rebase_u16<<<grid_for(size / 8 + 1, 256, 8), 256, 0, S(stream)>>>(levels, size, (unsigned)delta);
+    FQ_LAUNCHED("k_rebase_u16");
     return FQ_OK;
 }
 

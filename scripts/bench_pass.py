@@ -26,15 +26,17 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--opts", default="plan=0,1")
     ap.add_argument("--detail", action="store_true", help="per-pass CUDA-event times of one step")
+    ap.add_argument("--state", default="c128", choices=["c128", "c64"])
     args = ap.parse_args()
     n, p = args.n, args.p
-    sim = QaoaSimulator(terms=labs_terms(n))
+    dt = torch.complex64 if args.state == "c64" else torch.complex128
+    sim = QaoaSimulator(terms=labs_terms(n), dtype=dt)
     dc = sim.device_costs
     rng = np.random.default_rng(0)
     g, b = rng.uniform(0, 1, p), rng.uniform(0, 1, p)
-    state = torch.empty(1 << n, dtype=torch.complex128, device="cuda")
+    state = torch.empty(1 << n, dtype=dt, device="cuda")
     e = torch.empty(1, dtype=torch.float64, device="cuda")
-    S = 16 * (1 << n)
+    S = (8 if args.state == "c64" else 16) * (1 << n)
     C = dc.nbytes_per_amp() * (1 << n)
     opts = [o.split("=") for o in args.opts.split(";") if o]
     names = [o[0] for o in opts]
@@ -44,7 +46,7 @@ def main():
         for label, gam in (("phase", g), ("nophase", np.zeros(p))):
             layers = [(float(x), float(y), 1, 0, n) for x, y in zip(gam, b)]
             lay = (_lib.FqLayer * p)(*[_lib.FqLayer(*t) for t in layers])
-            passes = _lib.load().fq_plan_x_passes(n, p, lay)
+            passes = _lib.load().fq_plan_x_passes(n, p, lay, _lib.STATE_C64 if args.state == "c64" else 0)
             fn = lambda: run_program(state, n, "x", layers, dc=dc, init=True, init_amp=1 / math.sqrt(1 << n),
                                      expectation_out=e)
             for _ in range(3):

@@ -65,20 +65,27 @@ def test_no_cpu_fallback():
         QaoaSimulator(terms=labs_terms(4))
 
 
-def _plan(n, p):
+def _plan(n, p, state_kind=0):
     layers = (_lib.FqLayer * p)(*[_lib.FqLayer(0.1, 0.2, 1, 0, n) for _ in range(p)])
-    return _lib.load().fq_plan_x_passes(n, p, layers)
+    return _lib.load().fq_plan_x_passes(n, p, layers, state_kind)
 
 
 def test_pass_planner_counts():
-    # 3 qubit groups at n = 26 (12 + 7 + 7) -> 1 + 2p fused passes
+    # 3 qubit groups at n = 26 (7 + 12 + 7) -> 1 + 2p fused passes
     assert _plan(26, 10) == 21
     assert _plan(26, 1) == 3
-    # n = 13..22: two groups -> p + 1 passes
+    # n = 13..22: two groups -> p + 1 passes (n = 22: the state stays in L2, so a
+    # 10-target group with 4-amplitude runs costs nothing extra)
     assert _plan(16, 4) == 5
     assert _plan(22, 10) == 11
-    # n = 34 local 31: 12 + 10 + 9 -> 3 groups
-    assert _plan(31, 10) == 21
+    # complex64 halves the bytes per amplitude: n = 23 is still L2-resident
+    assert _plan(23, 10, _lib.STATE_C64) == 11
+    assert _plan(23, 10) == 21
+    # n = 34 local 31: 12 + 19 high targets; chunks of <= 10 would leave runs of
+    # 4-8 amplitudes (64-128 B), so the cost model takes 3 high chunks of 6-7
+    # targets (runs of >= 32 amplitudes) -> 4 groups, 1 + 3p passes
+    assert _plan(31, 10) == 31
+    assert _plan(31, 10, _lib.STATE_C64) == 31
     assert _plan(12, 4) == 1  # resident
 
 

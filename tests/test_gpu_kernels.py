@@ -212,3 +212,18 @@ def test_u16_levels_via_wht_chunks():
     dc2 = DeviceCosts.from_polynomial(labs_terms(22), keep_f64=False, index_base=3 << 20, n_local=20)
     ref2 = O.precompute_cost_vector(22, [(t.weight, t.support) for t in labs_terms(22).terms], base=3 << 20, size=1 << 20)
     np.testing.assert_array_equal(dc2.scale * dc2.u16.cpu().numpy().astype(np.float64) + dc2.offset, ref2)
+    # levels start at the observed minimum (phase tables sized by the range in use)
+    for d, r in ((dc, ref), (dc2, ref2)):
+        assert int(d.u16.cpu().numpy().min()) == 0 and d.offset == r.min()
+        assert d.levels == int(round((r.max() - r.min()) / d.scale)) + 1
+
+
+def test_rebase_u16():
+    from paper_2309_04841_b200 import _lib
+
+    rng = np.random.default_rng(5)
+    for size in (8, 4096 + 5, 1 << 16):
+        lv = rng.integers(300, 65535, size).astype(np.uint16)
+        t = torch.from_numpy(lv.view(np.int16)).cuda().view(torch.uint16)
+        _lib.call("fq_rebase_u16", t.data_ptr(), size, 300, _lib.stream())
+        np.testing.assert_array_equal(t.view(torch.int16).cpu().numpy().view(np.uint16), lv - 300)
