@@ -187,8 +187,9 @@ def main():
     ap.add_argument("--qubits", "--n", dest="n", type=int, default=0, help="total qubits (default 26 + log2 N)")
     ap.add_argument("--p", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
-    ap.add_argument("--global-mode", default="p2p", choices=["p2p", "exchange"],
-                    help="N>1: global-qubit mixer as one peer-memory kernel (p2p) or NCCL all-to-all exchanges")
+    ap.add_argument("--global-mode", default="fused", choices=["fused", "p2p", "exchange"],
+                    help="N>1: one sharded program whose global-qubit passes span all shards over peer memory "
+                         "(fused), a per-layer peer-memory global kernel (p2p), or NCCL all-to-all exchanges")
     ap.add_argument("--state", default="c128", choices=["c128", "c64"],
                     help="state type: complex128 (the headline, the reference's) or the optional complex64 (N=1)")
     args = ap.parse_args()
@@ -295,13 +296,19 @@ def main():
     if world == 1:
         tile_bytes = passes * 2 * S - S + (n_phase + 1) * Cb  # first pass generates |+>, last reads costs for E
         launches = passes + 1
+    elif args.global_mode == "fused":
+        # one sharded plan over all n qubits; its global-group passes span the shards
+        glay = (_lib.FqLayer * p)(*[_lib.FqLayer(float(gi), float(bi), 1, 0, n) for gi, bi in zip(g, b)])
+        gp = ctypes.c_int()
+        passes = _lib.load().fq_plan_sharded_passes(n_local, k, p, glay, ctypes.byref(gp))
+        tile_bytes = passes * 2 * S - S + (n_phase + 1) * Cb
+        launches = passes + 2 * gp.value + 1  # + two device barriers per spanning pass
+        nvlink_bytes = gp.value * 2 * S * (world - 1) // world
     else:
         post = p * (1 if k > 0 else 0)  # the k-position pass after each exchange
-        local_passes = passes * p if False else None
         per_layer = _lib.load().fq_plan_x_passes(n_local, 1, lay, skind)
         tile_bytes = p * per_layer * 2 * S - S + n_phase * Cb + post * 2 * S + S + Cb
         launches = p * (per_layer + (1 if k > 0 else 0)) + 2
-        del local_passes
     peak, peak_kind = load_peaks()
     achieved_step = tile_bytes / (ms_step / 1e3) / 1e9
 
@@ -417,10 +424,16 @@ def main():
                                       f"evaluations)" if world > 1 else ""),
                        "n": n, "p": p, "n_local": n_local, "angles": "default_rng(0) U(0,1)",
                        "cost_encoding": "uint16 levels (lossless)" if dc.u16 is not None else "float64",
-                       "l2": f"no flush: {S / 2**30:.1f} GiB state per GPU >> 126 MB L2",
+                       "l2": (f"no flush: {S / 2**30:.2f} GiB state per GPU >> 126 MB L2" if S > (256 << 20)
+                              else f"state of {S >> 20} MiB per GPU is L2-sized (validation sizes only)"),
                        "parallelism": (f"state sharded over {world} GPUs by global qubits, global-qubit mixer: "
-                                       f"{'peer-memory kernel (CUDA IPC over NVLink)' if args.global_mode == 'p2p' else 'NCCL all-to-all'}")
-                                      if world > 1 else "single GPU"},
+                                       + {"fused": "passes spanning all shards over peer memory (CUDA IPC, NVLink), "
+                                                   "fused across layers",
+                                          "p2p": "per-layer peer-memory kernel (CUDA IPC over NVLink)",
+                                          "exchange": "NCCL all-to-all"}[args.global_mode])
+                                      if world > 1 else "single GPU",
+                       **({"nvlink_bytes_per_step": nvlink_bytes, "spanning_passes_per_step": gp.value}
+                          if world > 1 and args.global_mode == "fused" else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                          "kernel": "k_pass16 (every tiled pass of the step; per-launch CUDA events)",

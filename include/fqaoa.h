@@ -150,10 +150,10 @@ int fq_masked_probability_c64(const void *psi, const void *costs, int cost_kind,
                               double offset, int64_t size, double cutoff, double *out_dev,
                               double *scratch, void *stream);
 
-/* levels[k] -= delta for every k (all levels >= delta): moves the level
- * origin to the diagonal's minimum after packing from a bound (decode offset
- * grows by delta*scale, exactly), so the phase tables cover the levels in use.
- * levels 16-B aligned. */
+/* levels[k] -= delta for every k (delta may be negative; the caller keeps
+ * every level in [0, 65535]): moves the level origin — to the diagonal's
+ * minimum after packing from a bound, or to a common origin across shards —
+ * with the decode offset moving by delta*scale, exactly.  levels 16-B aligned. */
 int fq_rebase_u16(uint16_t *levels, int64_t size, int delta, void *stream);
 
 /* Lossless uint16 packing of a float64 diagonal (terms.py:155-175):
@@ -214,6 +214,42 @@ int fq_qaoa_evolve_batched(int n, int mixer, const void *costs, int cost_kind, d
                            double offset, int p, int batch, const double *gammas,
                            const double *betas, const void *psi_init, void *psi_out,
                            double *out_dev, void *stream);
+
+/* A state sharded over K = 2^k ranks by its top k ("global") qubits
+ * (reference distributed.py:51-54): shard r holds global indices
+ * [r 2^n_local, (r+1) 2^n_local). */
+typedef struct fq_shard_desc {
+    int k;                          /* global qubits, 1..3 (K = 2..8 shards)                 */
+    int rank;                       /* this process's shard; -1: all K shards are this
+                                       process's (one device, one stream: the reference's
+                                       in-process worker model)                            */
+    void *const *shards;            /* [K] complex128 state shards as mapped in this process
+                                       (peers via fq_ipc_open)                               */
+    const void *const *costs;       /* [K] cost shards, one encoding / scale / offset        */
+    void *const *flags;             /* [K] peer flag arrays of fq_peer_barrier (rank >= 0)   */
+    unsigned *epoch;                /* host: last barrier epoch used; advanced by the call   */
+    int *barrier_err;               /* device error word of the barrier                      */
+} fq_shard_desc;
+
+/* The fused program on a sharded state (replaces the reference's per-layer
+ * Alg. 4 — local sweeps, all_to_all_exchange, k-position sweep, exchange —
+ * distributed.py:137-157): ONE plan over all n = n_local + k qubits.  Groups
+ * of local qubits run as ordinary passes on the rank's own shard; the group
+ * holding the k global qubits runs as one pass whose 2^12-amplitude tiles span
+ * all K shards over peer memory (NVLink), rank r taking 1/K of the tiles, with
+ * stream-ordered device barriers (fq_peer_barrier) before and after it.  Layer
+ * fusion works across the global group like any other, so global passes are
+ * about one per two layers, each moving (K-1)/K of its bytes over NVLink once.
+ * desc->n = n_local; desc->psi / desc->costs are ignored (shards / costs
+ * below); layer qubit ranges and the custom su2 table use global positions
+ * [0, n); desc->init_amp = 2^(-n/2); desc->expectation_dev receives this
+ * rank's partial sum (rank >= 0: all-reduce it) or the total (rank = -1).
+ * complex128, X and custom mixers, n_local >= 12. */
+int fq_qaoa_evolve_sharded(const fq_evolve_desc *desc, const fq_shard_desc *shards, void *stream);
+
+/* Pass count of fq_qaoa_evolve_sharded's plan and, in *global_passes, how many
+ * of them span the shards (peer-memory passes). */
+int fq_plan_sharded_passes(int n_local, int k, int n_layers, const fq_layer *layers, int *global_passes);
 
 /* Number of HBM passes fq_qaoa_evolve will run for an X-mixer program on a
  * state of state_kind (FQ_STATE_*; the plan depends on the bytes per

@@ -37,6 +37,13 @@ class FqEvolveDesc(ctypes.Structure):
     ]
 
 
+class FqShardDesc(ctypes.Structure):
+    _fields_ = [
+        ("k", I), ("rank", I), ("shards", ctypes.POINTER(P)), ("costs", ctypes.POINTER(P)),
+        ("flags", ctypes.POINTER(P)), ("epoch", ctypes.POINTER(ctypes.c_uint)), ("barrier_err", P),
+    ]
+
+
 _SIGS = {
     "fq_version": ([], I),
     "fq_last_error": ([], ctypes.c_char_p),
@@ -61,6 +68,8 @@ _SIGS = {
     "fq_compact_u16": ([P, P, I64, D, D, P, P], I),
     "fq_rebase_u16": ([P, I64, I, P], I),
     "fq_qaoa_evolve": ([ctypes.POINTER(FqEvolveDesc), P], I),
+    "fq_qaoa_evolve_sharded": ([ctypes.POINTER(FqEvolveDesc), ctypes.POINTER(FqShardDesc), P], I),
+    "fq_plan_sharded_passes": ([I, I, I, ctypes.POINTER(FqLayer), P], I),
     "fq_qaoa_evolve_batched": ([I, I, P, I, D, D, I, I, P, P, P, P, P, P], I),
     "fq_plan_x_passes": ([I, I, ctypes.POINTER(FqLayer), I], I),
     "fq_set_option": ([ctypes.c_char_p, I], I),

@@ -386,9 +386,27 @@ static double run_factor(long long run_bytes, bool heavy) {
     return heavy ? 8.0 : 4.7;
 }
 
-static double plan_cost(const std::vector<PlannedPass> &seq, const std::vector<Group> &gs, int n, int elem) {
+// Sharded states (fq_qaoa_evolve_sharded): the top kq of the n positions are
+// global qubits (the shard index).  A group holds all of them or none: its
+// tile then spans every shard (a peer-memory pass, G = true).
+static int global_count(const Group &g, int n, int kq) {
+    int c = 0;
+    for (int q : g.targets) c += q >= n - kq;
+    return c;
+}
+
+// A peer-memory pass moves (K-1)/K of its bytes over NVLink (~0.9 TB/s per
+// direction vs ~6.5 TB/s of HBM).
+constexpr double kGlobalPassCost = 5.0;
+
+static double plan_cost(const std::vector<PlannedPass> &seq, const std::vector<Group> &gs, int n, int elem,
+                        int kq = 0) {
+    for (auto &g : gs) {
+        const int c = global_count(g, n, kq);
+        if (c != 0 && c != kq) return 1e300;
+    }
     // a state that stays in L2 (126 MB) between passes does not see DRAM run lengths
-    const bool l2_resident = ((long long)elem << n) <= (64LL << 20);
+    const bool l2_resident = ((long long)elem << (n - kq)) <= (64LL << 20);
     double c = 0.0;
     for (auto &pp : seq) {
         if (pp.group < 0) {
@@ -396,22 +414,27 @@ static double plan_cost(const std::vector<PlannedPass> &seq, const std::vector<G
             continue;
         }
         const int sq = pass_seq(gs[pp.group], pp);
-        c += pass_cost(sq) * (l2_resident ? 1.0 : run_factor((long long)elem << run_bits_of(gs[pp.group]), seq_heavy(sq)));
+        double pc = pass_cost(sq) * (l2_resident ? 1.0 : run_factor((long long)elem << run_bits_of(gs[pp.group]), seq_heavy(sq)));
+        if (kq > 0 && global_count(gs[pp.group], n, kq) > 0) pc *= kGlobalPassCost;
+        c += pc;
     }
     return c;
 }
 
-// elem: bytes per amplitude (16 complex128, 8 complex64)
+// elem: bytes per amplitude (16 complex128, 8 complex64); kq: global qubits of a sharded state
 static std::vector<PlannedPass> plan_x(int n, int nl, const fq_layer *layers, std::vector<Group> &groups, bool fuse,
-                                       int elem) {
-    if (g_plan >= 0) return plan_with(n, nl, layers, groups, g_plan, g_plan == 0 ? 10 : 8, fuse);
+                                       int elem, int kq = 0) {
+    if (g_plan >= 0) {
+        auto seq = plan_with(n, nl, layers, groups, g_plan, g_plan == 0 ? 10 : 8, fuse);
+        if (plan_cost(seq, groups, n, elem, kq) < 1e299) return seq;  // else: search
+    }
     std::vector<PlannedPass> best;
     double best_cost = 1e300;
     for (int style = 0; style < 2; ++style) {
         for (int tmax = 12; tmax >= 4; --tmax) {
             std::vector<Group> gs;
             auto seq = plan_with(n, nl, layers, gs, style, tmax, fuse);
-            const double c = plan_cost(seq, gs, n, elem);
+            const double c = plan_cost(seq, gs, n, elem, kq);
             if (c < best_cost - 1e-9) {
                 best_cost = c;
                 best = seq;
@@ -467,31 +490,90 @@ static int launch_pass(int mix, int cost, bool c64, const PassParams &P, const P
                           : launch_pass_rx_f64_light(P, M, seq, ph, ma, mb, k, grid, st);
 }
 
-static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
-    const int n = d->n;
+// Sharded execution context (fq_qaoa_evolve_sharded); null for one state.
+struct ShardCtx {
+    int k = 0, K = 1;
+    int rank = 0;                          // -1: every shard belongs to this process (one stream)
+    void *const *shards = nullptr;         // [K] state shards as mapped in this process
+    const void *const *costs = nullptr;    // [K] cost shards
+    void *const *flags = nullptr;          // [K] peer barrier flag arrays (rank >= 0)
+    unsigned *epoch = nullptr;
+    int *err = nullptr;
+};
+
+static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCtx *sh = nullptr) {
+    const int nl = d->n;                      // qubits per shard (= n for one state)
+    const int kq = sh ? sh->k : 0;
+    const int nv = nl + kq;                   // qubits of the whole register
+    const int K = 1 << kq;
     std::vector<Group> groups;
     const bool c64 = d->state_kind == FQ_STATE_C64;
     const long long elem = c64 ? (long long)sizeof(float2) : (long long)sizeof(double2);
-    auto seq = plan_x(n, d->n_layers, d->layers, groups, g_fuse != 0, (int)elem);
+    const int CB = d->cost_kind == FQ_COST_F64 ? 8 : 2;
+    auto seq = plan_x(nv, d->n_layers, d->layers, groups, g_fuse != 0, (int)elem, kq);
     const int mix = (d->mixer == FQ_MIXER_X) ? MIX_RX : MIX_SU2;
-    const long long n_tiles = 1LL << (n - kTileBits);
+    const long long n_tiles = 1LL << (nl - kTileBits);  // per shard
     int table_hi = 0;
     if (d->cost_kind == FQ_COST_U16 && d->cost_levels > 0 && g_phase_tables) {
         const int rows = ((d->cost_levels - 1) >> 6) + 1;
         table_hi = rows <= kMaxTableHi ? rows : 0;
     }
     bool init_pending = d->init != 0;
-    void *psi = d->psi;
-    const long long size = 1LL << n;
+    // the shards this process works on: its own (rank), or all of them (in-process)
+    std::vector<int> mine;
+    if (!sh) mine.push_back(0);
+    else if (sh->rank >= 0) mine.push_back(sh->rank);
+    else for (int r = 0; r < K; ++r) mine.push_back(r);
+    auto shard_psi = [&](int r) -> void * { return sh ? sh->shards[r] : d->psi; };
+    auto shard_costs = [&](int r) -> const void * { return sh ? sh->costs[r] : d->costs; };
+    auto shard_desc = [&](int r) {
+        fq_evolve_desc e = *d;
+        e.psi = shard_psi(r);
+        e.costs = shard_costs(r);
+        return e;
+    };
+    const long long size = 1LL << nl;
     const int sms = sm_count() > 0 ? sm_count() : 148;
     const int grid = (int)std::min<long long>(n_tiles, (long long)sms * 2);
+    // expectation of several shards: per-shard sums in the top of the scratch, then one sum
+    double *const shard_sums = d->scratch ? d->scratch + FQ_SCRATCH_DOUBLES - 16 : nullptr;
+    auto expect_shards = [&]() -> int {
+        if (mine.size() == 1) {
+            fq_evolve_desc e = shard_desc(mine[0]);
+            return state_expectation(&e, e.psi, size, st);
+        }
+        for (size_t i = 0; i < mine.size(); ++i) {
+            fq_evolve_desc e = shard_desc(mine[i]);
+            e.expectation_dev = shard_sums + i;
+            if (int s = state_expectation(&e, e.psi, size, st)) return s;
+        }
+        k_sum_partials<<<1, 32, 0, st>>>(shard_sums, (int)mine.size(), d->expectation_dev);
+        FQ_LAUNCHED("k_sum_partials");
+        return FQ_OK;
+    };
+    auto init_shards = [&]() -> int {
+        for (int r : mine) {
+            fq_evolve_desc e = shard_desc(r);
+            if (int s = state_init(&e, e.psi, size, st)) return s;
+        }
+        return FQ_OK;
+    };
+    auto barrier = [&]() -> int {
+        if (!sh || sh->rank < 0) return FQ_OK;  // one stream orders everything
+        return fq_peer_barrier(sh->flags, K, sh->rank, ++*sh->epoch, sh->err, st);
+    };
 
     if (seq.empty()) {
-        if (init_pending) {
-            int s = state_init(d, psi, size, st);
-            if (s) return s;
+        if (d->n_layers > 0 && kq > 0) {
+            for (int l = 0; l < d->n_layers; ++l)
+                if (d->layers[l].q_hi > d->layers[l].q_lo) {
+                    set_error("fq_qaoa_evolve_sharded: no valid plan (the global qubits must share one group)");
+                    return FQ_ERR_UNSUPPORTED;
+                }
         }
-        if (d->expectation_dev) return state_expectation(d, psi, size, st);
+        if (init_pending)
+            if (int s = init_shards()) return s;
+        if (d->expectation_dev) return expect_shards();
         return FQ_OK;
     }
     g_last_plan.clear();
@@ -509,44 +591,61 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
     for (size_t si = 0; si < seq.size(); ++si) {
         const PlannedPass &pp = seq[si];
         const bool last = (si + 1 == seq.size());
-        if (pp.group < 0) {  // standalone phase
+        if (pp.group < 0) {  // standalone phase, shard-local
             g_last_plan.push_back({-1, 1, 0, init_pending ? 1 : 0, (last && d->expectation_dev) ? 1 : 0});
             if (init_pending) {
-                int s = state_init(d, psi, size, st);
-                if (s) return s;
+                if (int s = init_shards()) return s;
                 init_pending = false;
             }
             const fq_layer &L = d->layers[pp.phase_layer];
-            if (c64) launch_phase(static_cast<float2 *>(psi), d, size, L.gamma, st);
-            else launch_phase(static_cast<double2 *>(psi), d, size, L.gamma, st);
-            FQ_LAUNCHED("k_phase");
-            if (last && d->expectation_dev) {
-                int s = state_expectation(d, psi, size, st);
-                if (s) return s;
+            for (int r : mine) {
+                fq_evolve_desc e = shard_desc(r);
+                if (c64) launch_phase(static_cast<float2 *>(e.psi), &e, size, L.gamma, st);
+                else launch_phase(static_cast<double2 *>(e.psi), &e, size, L.gamma, st);
+                FQ_LAUNCHED("k_phase");
             }
+            if (last && d->expectation_dev)
+                if (int s = expect_shards()) return s;
             if (int s = mark(si + 1)) return s;
             continue;
         }
         const Group &g = groups[pp.group];
+        const int gq = global_count(g, nv, kq);
+        if (gq != 0 && gq != kq) {
+            set_error("fq_qaoa_evolve_sharded: a group holds %d of the %d global qubits", gq, kq);
+            return FQ_ERR_UNSUPPORTED;
+        }
+        const bool global = gq > 0;
         PassParams P;
         std::memset(&P, 0, sizeof P);
-        P.psi = psi;
-        P.costs = d->costs;
         P.cost_scale = d->cost_scale;
         P.cost_offset = d->cost_offset;
-        P.partials = d->scratch;
         P.init_amp = d->init_amp;
-        P.n_tiles = n_tiles;
         P.table_hi = table_hi;
-        for (int i = 0; i < kTileBits; ++i) P.tile_pos[i] = g.tile_pos[i];
+        // global tile bits (the top kq) carry no address: their tile_pos only
+        // inserts zeros above every local bit (tile_base)
+        for (int i = 0; i < kTileBits; ++i) P.tile_pos[i] = g.tile_pos[i] < nl ? g.tile_pos[i] : 62;
+        P.gbits = global ? kq : 0;
+        P.gshift = 8 - kq;
+        P.gmask = K - 1;
+        if (global)
+            for (int r = 0; r < K; ++r) {
+                P.sdelta[r] = static_cast<const char *>(sh->shards[r]) - static_cast<const char *>(sh->shards[0]);
+                P.cdelta[r] = static_cast<const char *>(sh->costs[r]) - static_cast<const char *>(sh->costs[0]);
+            }
         for (int pat = 0; pat < 3; ++pat) {
             const int f = pat_first_bit(pat);
             for (int i = 0; i < kRegs; ++i) {
                 long long o = 0;
-                for (int j = 0; j < 4; ++j)
-                    if ((i >> j) & 1) o += 1LL << g.tile_pos[f + j];
-                P.roff[pat][i] = o * elem;
-                P.coff[pat][i] = o * (d->cost_kind == FQ_COST_F64 ? 8 : 2);
+                int shard = 0;
+                for (int j = 0; j < 4; ++j) {
+                    if (!((i >> j) & 1)) continue;
+                    const int q = g.tile_pos[f + j];
+                    if (q < nl) o += 1LL << q;
+                    else shard |= 1 << (q - nl);  // global bit (PAT8 registers only)
+                }
+                P.roff[pat][i] = o * elem + (global ? P.sdelta[shard] : 0);
+                P.coff[pat][i] = o * CB + (global ? P.cdelta[shard] : 0);
             }
         }
         P.init = init_pending ? 1 : 0;
@@ -572,7 +671,7 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
                 fscale *= std::pow(f, ntarget);
             } else {
                 for (int i = 0; i < kTileBits; ++i) {
-                    const double *c4 = d->su2 + ((size_t)layer * n + g.tile_pos[i]) * 4;
+                    const double *c4 = d->su2 + ((size_t)layer * nv + g.tile_pos[i]) * 4;
                     C.a[i] = make_double2(c4[0], c4[1]);
                     C.b[i] = make_double2(c4[2], c4[3]);
                 }
@@ -582,38 +681,77 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st) {
         if (two) fill(pp.layerB, P.B);
         P.final_scale = fscale;
         P.tile_mask = 0;
-        for (int i = 0; i < kTileBits; ++i) P.tile_mask |= 1LL << g.tile_pos[i];
+        for (int i = 0; i < kTileBits; ++i)
+            if (g.tile_pos[i] < nl) P.tile_mask |= 1LL << g.tile_pos[i];
         P.step_dep = deposit(grid, P.tile_mask);
         P.reverse = g_zigzag ? (int)(si & 1) : 0;
-        // the tensor prefetch pays for long runs only: with short runs its many
-        // small requests compete with the demand loads (measured, n = 28..34)
-        P.pf_dist = g_prefetch >= 0 ? g_prefetch : ((elem << run_bits_of(g)) >= 256 ? 1 : 0);
         P.probe = g_probe;
         P.run_bits = 0;
         while (P.run_bits < kTileBits && g.tile_pos[P.run_bits] == P.run_bits) ++P.run_bits;
         P.pf_cost = (ph != 0 || P.expect) ? 1 : 0;
-        PassMaps M;
-        std::memset(&M, 0, sizeof M);
-        if (P.pf_dist > 0) {
-            P.sm_rank = c64 ? cached_tile_map(&M.state, psi, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 2,
-                                              P.sm_shift, P.sm_bits)
-                            : cached_tile_map(&M.state, psi, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2,
-                                              P.sm_shift, P.sm_bits);
-            if (P.pf_cost)
-                P.cm_rank = d->cost_kind == FQ_COST_F64
-                                ? cached_tile_map(&M.cost, d->costs, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 1,
-                                                 P.cm_shift, P.cm_bits)
-                                : cached_tile_map(&M.cost, d->costs, n, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, 1,
-                                                 P.cm_shift, P.cm_bits);
-            if (P.sm_rank == 0 && P.cm_rank == 0) P.pf_dist = 0;
-        }
         const int ma = P.A.mode, mb = two ? P.B.mode : 2;
         if (P.expect && ph == 0 && !two && !seq_heavy(sq)) ph = 3;  // preload the expectation's costs
-        const int s = launch_pass(mix, d->cost_kind, c64, P, M, sq, ph, ma, mb, grid, st);
-        if (s) return s;
+        int launches = 0;
+        if (global) {
+            // one pass over every shard: rank r takes its 1/K of the tiles (in-process: all)
+            if (int s = barrier()) return s;
+            const long long T = 1LL << (nv - kTileBits);
+            const bool all = sh->rank < 0;
+            P.psi = sh->shards[0];
+            P.costs = sh->costs[0];
+            P.tile0 = all ? 0 : (T / K) * sh->rank;
+            P.n_tiles = all ? T : T / K;
+            P.partials = d->scratch;
+            P.pf_dist = 0;  // the tile spans several allocations: no single tensor map
+            PassMaps M;
+            std::memset(&M, 0, sizeof M);
+            const int ggrid = (int)std::min<long long>(P.n_tiles, (long long)sms * 2);
+            P.step_dep = deposit(ggrid, P.tile_mask);
+            int k = mask_class(sq, P.maskA);
+            int mbv = (mix == MIX_RX && !seq_heavy(sq) && mb != 2) ? 3 : mb;
+            if (mix == MIX_SU2) mbv = mb == 2 ? 2 : 3;
+            const int s = d->cost_kind == FQ_COST_U16
+                              ? launch_pass_global_u16(mix, P, M, sq, ph, mix == MIX_SU2 ? 0 : ma, mbv, k, ggrid, st)
+                              : launch_pass_global_f64(mix, P, M, sq, ph, mix == MIX_SU2 ? 0 : ma, mbv, k, ggrid, st);
+            if (s) return s;
+            launches = ggrid;
+            if (int s2 = barrier()) return s2;
+        } else {
+            P.n_tiles = n_tiles;
+            P.tile0 = 0;
+            // the tensor prefetch pays for long runs only: with short runs its many
+            // small requests compete with the demand loads (measured, n = 28..34)
+            const int pf = g_prefetch >= 0 ? g_prefetch : ((elem << run_bits_of(g)) >= 256 ? 1 : 0);
+            for (size_t mi = 0; mi < mine.size(); ++mi) {
+                const int r = mine[mi];
+                P.psi = shard_psi(r);
+                P.costs = shard_costs(r);
+                P.partials = d->scratch + launches;
+                P.pf_dist = pf;
+                P.sm_rank = P.cm_rank = 0;
+                PassMaps M;
+                std::memset(&M, 0, sizeof M);
+                if (P.pf_dist > 0) {
+                    P.sm_rank = c64 ? cached_tile_map(&M.state, P.psi, nl, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                                                      2, P.sm_shift, P.sm_bits)
+                                    : cached_tile_map(&M.state, P.psi, nl, g.tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
+                                                      2, P.sm_shift, P.sm_bits);
+                    if (P.pf_cost)
+                        P.cm_rank = d->cost_kind == FQ_COST_F64
+                                        ? cached_tile_map(&M.cost, P.costs, nl, g.tile_pos,
+                                                         CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 1, P.cm_shift, P.cm_bits)
+                                        : cached_tile_map(&M.cost, P.costs, nl, g.tile_pos,
+                                                         CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, 1, P.cm_shift, P.cm_bits);
+                    if (P.sm_rank == 0 && P.cm_rank == 0) P.pf_dist = 0;
+                }
+                const int s = launch_pass(mix, d->cost_kind, c64, P, M, sq, ph, ma, mb, grid, st);
+                if (s) return s;
+                launches += grid;
+            }
+        }
         g_last_plan.push_back({sq, ph, (int)g.targets.size(), P.init, P.expect});
         if (P.expect) {
-            k_sum_partials<<<1, 32, 0, st>>>(d->scratch, grid, d->expectation_dev);
+            k_sum_partials<<<1, 32, 0, st>>>(d->scratch, launches, d->expectation_dev);
             FQ_LAUNCHED("k_sum_partials");
         }
         if (int s2 = mark(si + 1)) return s2;
@@ -790,6 +928,50 @@ int fq_qaoa_evolve(const fq_evolve_desc *d, void *stream) {
     }
     if (d->mixer == FQ_MIXER_XY_RING || d->mixer == FQ_MIXER_XY_COMPLETE) return run_xy_program(d, st);
     return run_x_program(d, st);
+}
+
+int fq_qaoa_evolve_sharded(const fq_evolve_desc *d, const fq_shard_desc *s, void *stream) {
+    FQ_CHECK_ARG(d && s, "fq_qaoa_evolve_sharded: null descriptor");
+    FQ_CHECK_ARG(s->k >= 1 && s->k <= 3, "fq_qaoa_evolve_sharded: k=%d must be in [1, 3]", s->k);
+    const int K = 1 << s->k;
+    FQ_CHECK_ARG(s->rank >= -1 && s->rank < K, "fq_qaoa_evolve_sharded: bad rank %d", s->rank);
+    FQ_CHECK_ARG(d->n >= kTileBits && d->n + s->k <= 40, "fq_qaoa_evolve_sharded: n_local=%d must be >= %d", d->n,
+                 kTileBits);
+    FQ_CHECK_ARG(d->state_kind == FQ_STATE_C128, "fq_qaoa_evolve_sharded: complex128 states only");
+    FQ_CHECK_ARG(d->mixer == FQ_MIXER_X || d->mixer == FQ_MIXER_CUSTOM,
+                 "fq_qaoa_evolve_sharded: X or custom mixers (XY mixers use the exchange path)");
+    FQ_CHECK_ARG(d->mixer != FQ_MIXER_CUSTOM || d->su2, "fq_qaoa_evolve_sharded: custom mixer needs su2 table");
+    FQ_CHECK_ARG(d->n_layers >= 0 && (d->n_layers == 0 || d->layers), "fq_qaoa_evolve_sharded: bad layers");
+    FQ_CHECK_ARG(d->cost_kind == FQ_COST_F64 || d->cost_kind == FQ_COST_U16, "fq_qaoa_evolve_sharded: bad cost kind");
+    FQ_CHECK_ARG(d->scratch, "fq_qaoa_evolve_sharded: needs scratch");
+    FQ_CHECK_ARG(s->shards && s->costs, "fq_qaoa_evolve_sharded: null shard tables");
+    for (int r = 0; r < K; ++r)
+        FQ_CHECK_ARG(s->shards[r] && s->costs[r], "fq_qaoa_evolve_sharded: null shard %d", r);
+    FQ_CHECK_ARG(s->rank < 0 || (s->flags && s->epoch && s->barrier_err),
+                 "fq_qaoa_evolve_sharded: a rank needs the peer barrier (flags, epoch, error word)");
+    ShardCtx ctx;
+    ctx.k = s->k;
+    ctx.K = K;
+    ctx.rank = s->rank;
+    ctx.shards = s->shards;
+    ctx.costs = s->costs;
+    ctx.flags = s->flags;
+    ctx.epoch = s->epoch;
+    ctx.err = s->barrier_err;
+    return run_x_program(d, static_cast<cudaStream_t>(stream), &ctx);
+}
+
+int fq_plan_sharded_passes(int n_local, int k, int n_layers, const fq_layer *layers, int *global_passes) {
+    if (global_passes) *global_passes = 0;
+    if (n_local < kTileBits || k < 1 || k > 3) return -1;
+    std::vector<Group> groups;
+    const int nv = n_local + k;
+    auto seq = plan_x(nv, n_layers, layers, groups, g_fuse != 0, 16, k);
+    int gp = 0;
+    for (auto &pp : seq)
+        if (pp.group >= 0 && global_count(groups[pp.group], nv, k) > 0) ++gp;
+    if (global_passes) *global_passes = gp;
+    return (int)seq.size();
 }
 
 int fq_set_option(const char *name, int value) {

@@ -333,19 +333,22 @@ __global__ void k_compact_u16(uint16_t *__restrict__ out, const double *__restri
     }
 }
 
-// levels[k] -= delta, 8 levels per thread-iteration (16-B loads/stores)
-__global__ void k_rebase_u16(uint16_t *__restrict__ lv, int64_t size, unsigned delta) {
+// levels[k] -= delta (delta < 0: += -delta), 8 levels per thread-iteration
+// (16-B loads/stores).  Lane-wise 16-bit arithmetic in 32-bit words: the caller
+// guarantees no level leaves [0, 65535], so no borrow / carry crosses a lane.
+__global__ void k_rebase_u16(uint16_t *__restrict__ lv, int64_t size, int delta) {
     const int64_t n8 = size >> 3;
     uint4 *v = reinterpret_cast<uint4 *>(lv);
-    const unsigned d2 = delta | (delta << 16);
+    const unsigned a = (unsigned)(delta < 0 ? -delta : delta), d2 = a | (a << 16);
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n8; k += (int64_t)gridDim.x * blockDim.x) {
-        uint4 x = v[k];  // lane-wise 16-bit subtraction: every level >= delta, no borrows
-        x.x -= d2, x.y -= d2, x.z -= d2, x.w -= d2;
+        uint4 x = v[k];
+        if (delta >= 0) x.x -= d2, x.y -= d2, x.z -= d2, x.w -= d2;
+        else x.x += d2, x.y += d2, x.z += d2, x.w += d2;
         v[k] = x;
     }
     for (int64_t k = (n8 << 3) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < size;
          k += (int64_t)gridDim.x * blockDim.x)
-        lv[k] = (uint16_t)(lv[k] - delta);
+        lv[k] = (uint16_t)((int)lv[k] - delta);
 }
 
 }  // namespace fq
@@ -581,10 +584,11 @@ int fq_cost_minmax(const void *costs, int cost_kind, double scale, double offset
 }
 
 int fq_rebase_u16(uint16_t *levels, int64_t size, int delta, void *stream) {
-    FQ_CHECK_ARG(levels && size > 0 && delta >= 0 && delta <= 65535 && (reinterpret_cast<uintptr_t>(levels) & 15) == 0,
+    FQ_CHECK_ARG(levels && size > 0 && delta >= -65535 && delta <= 65535 &&
+                     (reinterpret_cast<uintptr_t>(levels) & 15) == 0,
                  "fq_rebase_u16: bad args");
     if (delta == 0) return FQ_OK;
-    k_rebase_u16<<<grid_for(size / 8 + 1, 256, 8), 256, 0, S(stream)>>>(levels, size, (unsigned)delta);
+    k_rebase_u16<<<grid_for(size / 8 + 1, 256, 8), 256, 0, S(stream)>>>(levels, size, delta);
     FQ_LAUNCHED("k_rebase_u16");
     return FQ_OK;
 }

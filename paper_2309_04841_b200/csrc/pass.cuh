@@ -90,6 +90,16 @@ struct PassParams {
     long long step_dep;       // pdep(gridDim.x) into the non-tile positions: base(t + grid) = next_base(base(t))
     int reverse;              // walk the tiles from the top (alternate passes: L2 reuse)
     CoefSet A, B;
+    // sharded state (G = true passes): the tile's top k tile bits are the k global
+    // qubits, i.e. the shard index.  psi / costs point at shard 0's mapping in
+    // this process and sdelta[s] / cdelta[s] are shard s's byte offsets from it
+    // (peer allocations: not additive over the global bits, so they enter as
+    // whole per-shard offsets: register offsets of PAT8, thread offsets of PAT4).
+    long long tile0;          // first tile of this launch (rank r: its 1/K of the tiles)
+    int gbits;                // k: tile bits 12-k..11 are the global qubits (their tile_pos is unused)
+    int gshift;               // PAT4: shard index = (tid >> gshift) & gmask
+    int gmask;
+    long long sdelta[8], cdelta[8];
 };
 
 constexpr int kTableLo = 64;     // low-table rows (6 level bits)
@@ -119,8 +129,9 @@ __host__ __device__ constexpr int pat_step(int i) {
     return PAT == PAT8 ? 272 * i : (PAT == PAT0 ? i : 17 * i);
 }
 
-// physical offset of this thread's element 0 for pattern PAT
-template <int PAT>
+// physical offset of this thread's element 0 for pattern PAT (G: the global
+// tile bits contribute through the shard offsets instead)
+template <int PAT, bool G = false>
 __device__ __forceinline__ long long thread_offset(const PassParams &P, int tid) {
     long long off = 0;
 #pragma unroll
@@ -129,6 +140,7 @@ __device__ __forceinline__ long long thread_offset(const PassParams &P, int tid)
         if (PAT == PAT8) tb = j;
         else if (PAT == PAT0) tb = 4 + j;
         else tb = (j < 4) ? j : j + 4;
+        if (G && tb >= kTileBits - P.gbits) continue;
         if ((tid >> j) & 1) off += 1LL << P.tile_pos[tb];
     }
     return off;
@@ -370,7 +382,7 @@ __device__ __forceinline__ int round_mask(const unsigned char *rt, int r) {
 //   K: target-mask class of the rounds (see round_mask): compile-time masks keep
 //       the butterfly code branch-free (run-time masks force register moves at
 //       every merge point).
-template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R = double>
+template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R = double, bool G = false>
 __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ PassParams P,
                                                         const __grid_constant__ CUtensorMap tm_state,
                                                         const __grid_constant__ CUtensorMap tm_cost) {
@@ -393,9 +405,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
         if (P.table_hi > 0) build_phase_tables<R>(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
         __syncthreads();
     }
-    const long long thr8 = thread_offset<PAT8>(P, tid);
-    const long long thr4 = thread_offset<PAT4>(P, tid);
+    constexpr int CB = COST == FQ_COST_F64 ? 8 : 2;
+    const long long thr8 = thread_offset<PAT8, G>(P, tid);
+    const long long thr4 = thread_offset<PAT4, G>(P, tid);
     const long long thrL = LAST == PAT8 ? thr8 : thr4;
+    // G: PAT4's thread bits include the shard index (PAT8's never do): this
+    // thread's shard byte offsets in the state / cost vector (0 otherwise),
+    // re-read from the parameter bank at each use (not held in registers)
+    auto g4s = [&]() -> long long {
+        if constexpr (G) return P.sdelta[(tid >> P.gshift) & P.gmask];
+        else return 0;
+    };
+    auto g4c = [&]() -> long long {
+        if constexpr (G) return P.cdelta[(tid >> P.gshift) & P.gmask];
+        else return 0;
+    };
     double eacc = 0.0;
 
     const bool pf = P.pf_dist > 0 && tid == 0;
@@ -405,10 +429,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
             if (tp < P.n_tiles) prefetch_tile(P, &tm_state, &tm_cost, P.reverse ? P.n_tiles - 1 - tp : tp, !P.init);
         }
     }
-    constexpr int CB = COST == FQ_COST_F64 ? 8 : 2;
     // reverse passes walk the tiles from the top: the previous pass ended there,
     // so the first tiles read are still in L2 (written moments ago)
-    long long base = tile_base(P, P.reverse ? P.n_tiles - 1 - blockIdx.x : blockIdx.x);
+    long long base = tile_base(P, P.tile0 + (P.reverse ? P.n_tiles - 1 - blockIdx.x : blockIdx.x));
     for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x,
                    base = P.reverse ? prev_base(base, P.tile_mask, P.step_dep) : next_base(base, P.tile_mask, P.step_dep)) {
         if (pf) {
@@ -433,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
             for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c8 + P.coff[PAT8][i]);
         }
         if (PH == 3) {  // the program's last pass: its expectation costs, in the store pattern
-            const char *cl = cs + thrL * CB;
+            const char *cl = cs + thrL * CB + (LAST == PAT8 ? 0 : g4c());
 #pragma unroll
             for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i]);
         }
@@ -442,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
 #pragma unroll
                 for (int i = 0; i < kRegs; ++i) raw[i] = (CostRaw<COST>)((tid * 7 + i * 131) & 1023);
             } else {
-                const char *c4 = cs + thr4 * CB;
+                const char *c4 = cs + thr4 * CB + g4c();
 #pragma unroll
                 for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c4 + P.coff[PAT4][i]);
             }
@@ -498,11 +521,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
         // ---- store (+ expectation) in the last round's pattern
         const R fs = (R)P.final_scale;
         if (PH != 3 && P.expect) {  // cost entries of the last pattern (final pass with a phase)
-            const char *cl = cs + thrL * CB;
+            const char *cl = cs + thrL * CB + (LAST == PAT8 ? 0 : g4c());
 #pragma unroll
             for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i]);
         }
-        char *psl = reinterpret_cast<char *>(static_cast<T *>(P.psi) + base + thrL);
+        char *psl = reinterpret_cast<char *>(static_cast<T *>(P.psi) + base + thrL) + (LAST == PAT8 ? 0 : g4s());
 #pragma unroll
         for (int i = 0; i < kRegs; ++i) {
             T x = v[i];
@@ -523,18 +546,18 @@ struct PassMaps {
     alignas(64) CUtensorMap cost;
 };
 
-template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R = double>
+template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R = double, bool G = false>
 static int launch_pass16(const PassParams &P, const PassMaps &M, int grid, cudaStream_t st) {
     static bool configured = false;
     constexpr int CP = table_copies<R>();
     const size_t smem = (size_t)(kTilePadded + (kTableLo + kMaxTableHi) * CP) * sizeof(C2<R>);
     if (!configured) {
-        cudaFuncSetAttribute(k_pass16<MIX, COST, SEQ, PH, MA, MB, K, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_pass16<MIX, COST, SEQ, PH, MA, MB, K, R, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         configured = true;
     }
     const size_t need = (size_t)(kTilePadded + (kTableLo + P.table_hi) * CP) * sizeof(C2<R>);
-    k_pass16<MIX, COST, SEQ, PH, MA, MB, K, R><<<grid, kThreads, need, st>>>(P, M.state, M.cost);
+    k_pass16<MIX, COST, SEQ, PH, MA, MB, K, R, G><<<grid, kThreads, need, st>>>(P, M.state, M.cost);
     FQ_LAUNCHED("k_pass16");
     return FQ_OK;
 }
@@ -543,18 +566,18 @@ static int launch_pass16(const PassParams &P, const PassMaps &M, int grid, cudaS
 // ph/ma/mb/k as the k_pass16 parameters (ma/mb already normalised by the
 // caller); a mask class k without an instantiation runs with the run-time
 // masks (K_RUNTIME), which PassParams always carries.
-template <int MIX, int COST, int SEQ, typename R = double>
+template <int MIX, int COST, int SEQ, typename R = double, bool G = false>
 static int select_seq(const PassParams &P, const PassMaps &M, int ph, int ma, int mb, int k, int grid, cudaStream_t st) {
     constexpr bool kHigh = SEQ == SEQ_84 || SEQ == SEQ_848;
 #define FQ_K(PHV, MAV, MBV)                                                                                  \
     if (ph == PHV && ma == MAV && mb == MBV) {                                                               \
-        if (k == K_FULL) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_FULL, R>(P, M, grid, st);          \
+        if (k == K_FULL) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_FULL, R, G>(P, M, grid, st);   \
         if constexpr (kHigh && MIX == MIX_RX) {                                                              \
-            if (k == 1) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 1, R>(P, M, grid, st);                \
-            if (k == 2) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 2, R>(P, M, grid, st);                \
-            if (k == 3) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 3, R>(P, M, grid, st);                \
+            if (k == 1) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 1, R, G>(P, M, grid, st);         \
+            if (k == 2) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 2, R, G>(P, M, grid, st);         \
+            if (k == 3) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 3, R, G>(P, M, grid, st);         \
         }                                                                                                    \
-        return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_RUNTIME, R>(P, M, grid, st);                        \
+        return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_RUNTIME, R, G>(P, M, grid, st);                 \
     }
     if constexpr (seq_heavy(SEQ)) {
         if constexpr (MIX == MIX_RX) {
@@ -577,9 +600,12 @@ int launch_pass_rx_u16_heavy(const PassParams &P, const PassMaps &M, int seq, in
 int launch_pass_rx_f64_light(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
 int launch_pass_rx_f64_heavy(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
 int launch_pass_su2(const PassParams &P, const PassMaps &M, int cost, int seq, int ph, int mb, int k, int grid, cudaStream_t st);
-// complex64 states (R = float): X mixer, all round programs, one unit per cost encoding
-int launch_pass_c64_u16(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
-int launch_pass_c64_f64(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
+// sharded states (G = true, complex128): passes whose tile spans the global
+// qubits; every mixer and round program, one unit per cost encoding (pass_global_*.cu)
+int launch_pass_global_u16(int mix, const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k,
+                           int grid, cudaStream_t st);
+int launch_pass_global_f64(int mix, const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k,
+                           int grid, cudaStream_t st);
 // complex64 states (R = float): X mixer, all round programs, one unit per cost encoding
 int launch_pass_c64_u16(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
 int launch_pass_c64_f64(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);

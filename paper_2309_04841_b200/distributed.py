@@ -20,6 +20,7 @@ Two deployments of the same orchestration:
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 from math import comb, sqrt
 from typing import Sequence
@@ -290,6 +291,53 @@ def global_su2_pass(shard_ptrs: Sequence[int], k: int, shard_size: int, part: in
     _lib.call("fq_global_su2_pass", ptrs, k, shard_size, part, parts, coef.ctypes.data, _lib.stream())
 
 
+def evolve_sharded(shard_ptrs: Sequence[int], cost_ptrs: Sequence[int], costs: DeviceCosts, n: int, k: int,
+                   mixer: Mixer, params: QaoaParams, init: bool, rank: int = -1, flags=None, epoch=None,
+                   err_ptr: int | None = None, expectation_out: torch.Tensor | None = None) -> None:
+    """libfqaoa fq_qaoa_evolve_sharded: the whole p-layer program on a state
+    sharded by its top k qubits — local groups as passes on each shard, the
+    global group as peer-memory passes over all shards, fused across layers.
+    ``rank`` -1: every shard is this process's (one stream, no barriers);
+    else this rank's shard plus the peer barrier (``flags``, ``epoch``, ``err_ptr``)."""
+    K = 1 << k
+    nl = n - k
+    dc = costs
+    arr = (_lib.FqLayer * max(1, params.p))(*[_lib.FqLayer(float(g), float(b), 1, 0, n)
+                                              for g, b in zip(params.gammas, params.betas)])
+    desc = _lib.FqEvolveDesc()
+    desc.n = nl
+    if dc.u16 is not None:
+        desc.cost_kind, desc.cost_scale, desc.cost_offset, desc.cost_levels = _lib.COST_U16, dc.scale, dc.offset, dc.levels
+    else:
+        desc.cost_kind, desc.cost_scale, desc.cost_offset, desc.cost_levels = _lib.COST_F64, 1.0, 0.0, 0
+    desc.mixer = _lib.MIXER_CODES[mixer.kind]
+    desc.n_layers = params.p
+    desc.layers = arr
+    su2 = mixer.su2_table(params.betas, n) if mixer.kind == "custom" else None
+    su2_keep = None
+    if su2 is not None:
+        su2_keep = np.ascontiguousarray(su2, dtype=np.float64)
+        desc.su2 = su2_keep.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    desc.init = 1 if init else 0
+    desc.init_amp = 1.0 / sqrt(float(2 ** n)) if init else 0.0
+    desc.expectation_dev = expectation_out.data_ptr() if expectation_out is not None else None
+    desc.scratch = _lib.scratch().data_ptr()
+    sd = _lib.FqShardDesc()
+    sd.k = k
+    sd.rank = rank
+    shards = (ctypes.c_void_p * K)(*shard_ptrs)
+    cps = (ctypes.c_void_p * K)(*cost_ptrs)
+    sd.shards, sd.costs = shards, cps
+    if rank >= 0:
+        fl = (ctypes.c_void_p * K)(*flags)
+        sd.flags = fl
+        sd.epoch = ctypes.pointer(epoch)
+        sd.barrier_err = err_ptr
+    _lib.check(_lib.load().fq_qaoa_evolve_sharded(ctypes.byref(desc), ctypes.byref(sd), _lib.stream()),
+               "fq_qaoa_evolve_sharded")
+    del su2_keep
+
+
 def simulate_qaoa_distributed(problem, params: QaoaParams, K: int, mixer: "str | Mixer" = "x",
                               initial=None, fused: bool = True) -> DistributedResult:
     """K logical workers on the current GPU (reference distributed.py:280-296).
@@ -305,6 +353,15 @@ def simulate_qaoa_distributed(problem, params: QaoaParams, K: int, mixer: "str |
     sharded = ShardedState(n, k, list(state.view(K, -1).unbind(0)))
     sc = ShardedCosts(n, k, _slice_device_costs(dc, K))
     n_local = n - k
+    if fused and 1 <= k <= 3 and n_local >= 12 and mixer.kind in ("x", "custom"):
+        # one sharded program: the global group's passes span the K shard views
+        # (the same kernels a multi-GPU rank runs over peer memory)
+        cost_t = [c.u16 if c.u16 is not None else c.f64 for c in sc.shards]
+        evolve_sharded([s.data_ptr() for s in sharded.shards], [t.data_ptr() for t in cost_t], sc.shards[0], n, k,
+                       mixer, params, init, rank=-1)
+        sharded.exchange_count += 2 * params.p  # the reference's logical count (Alg. 4)
+        instrumentation.bump("exchange", 2 * params.p)
+        return DistributedResult(sharded, sc, dc)
     for gamma, beta in zip(params.gammas, params.betas):
         if mixer.kind == "custom" and k > 0 and fused and k <= 4:
             us = list(mixer.su2_factory(beta))
@@ -368,15 +425,18 @@ class ShardedQaoaSimulator:
         self.chunk_bytes = chunk_bytes
         self._state = None
         self._spare = None
-        if global_mode not in ("exchange", "p2p"):
-            raise ValueError(f"global_mode must be 'exchange' or 'p2p', got {global_mode!r}")
+        if global_mode not in ("exchange", "p2p", "fused"):
+            raise ValueError(f"global_mode must be 'exchange', 'p2p' or 'fused', got {global_mode!r}")
         self.global_mode = global_mode
         self.device_barrier = device_barrier
         self._p2p_buf = None
         self._peers: list[int] | None = None
         self._flag_ptrs: list[int] | None = None
+        self._cost_peers: list[int] | None = None
         self._opened: list[tuple[int, int]] = []
-        self._epoch = 0
+        self._epoch = ctypes.c_uint(0)
+        if global_mode == "fused" and self.k > 0:
+            self._common_cost_encoding()
 
     # ------------------------------------------------------------------ exchange
     def exchange(self, shard: torch.Tensor) -> torch.Tensor:
@@ -433,6 +493,8 @@ class ShardedQaoaSimulator:
         if self.mixer.preserves_hamming_weight:
             return self._simulate_xy(params, initial_weight, expectation)
         nl, k = self.n_local, self.k
+        if self.global_mode == "fused" and k > 0:
+            return self._simulate_fused(params, initial_weight, expectation)
         if self.global_mode == "p2p" and k > 0:
             psi = self._p2p_shard()
             if initial_weight is not None:
@@ -484,8 +546,6 @@ class ShardedQaoaSimulator:
 
     def _map_peers(self, ptr: int) -> list[int]:
         """All-gather the CUDA IPC handle of a local buffer; map every peer's."""
-        import ctypes
-
         h = (ctypes.c_char * 64)()
         off = ctypes.c_int64()
         _lib.call("fq_ipc_handle", ptr, h, ctypes.byref(off))
@@ -507,11 +567,9 @@ class ShardedQaoaSimulator:
         flag barrier in peer memory (fq_peer_barrier, no host sync), or host
         synchronisation + dist.barrier."""
         if self.device_barrier:
-            import ctypes
-
-            self._epoch += 1
+            self._epoch.value += 1
             ptrs = (ctypes.c_void_p * self.K)(*self._flag_ptrs)
-            _lib.call("fq_peer_barrier", ptrs, self.K, self.rank, self._epoch,
+            _lib.call("fq_peer_barrier", ptrs, self.K, self.rank, self._epoch.value,
                       self._flags.data_ptr() + 4 * self.K, _lib.stream())
         else:
             torch.cuda.synchronize()
@@ -532,6 +590,66 @@ class ShardedQaoaSimulator:
         self._barrier()
         self.exchange_count += 2
         instrumentation.bump("exchange", 2)
+
+    # ------------------------------------------------------------------ fused sharded program
+    def _common_cost_encoding(self) -> None:
+        """Peer-memory passes decode any shard's costs with one (scale,
+        offset): uint16 shards agree on the scale and move to the global
+        minimum as origin (fq_rebase_u16), else every shard uses float64."""
+        dc = self.costs
+        mine = (dc.u16 is not None, dc.f64 is not None, dc.scale, dc.offset,
+                dc.offset + (dc.levels - 1) * dc.scale if dc.u16 is not None else 0.0)
+        allv = [None] * self.K
+        dist.all_gather_object(allv, mine, group=self.group)
+        if all(v[0] for v in allv) and len({v[2] for v in allv}) == 1:
+            scale = allv[0][2]
+            lo = min(v[3] for v in allv)
+            hi = max(v[4] for v in allv)
+            levels = int(round((hi - lo) / scale)) + 1
+            if levels <= 65536:
+                delta = int(round((dc.offset - lo) / scale))
+                if delta:
+                    _lib.call("fq_rebase_u16", dc.u16.data_ptr(), dc.u16.numel(), -delta, _lib.stream())
+                dc.offset = lo
+                dc.levels = levels
+                self._cost_kind = _lib.COST_U16
+                return
+        if not all(v[1] for v in allv):
+            raise MemoryError("sharded cost encodings disagree and the float64 diagonal was not kept "
+                              "(use global_mode='p2p' or 'exchange')")
+        self._cost_kind = _lib.COST_F64
+
+    def _cost_tensor(self) -> torch.Tensor:
+        return self.costs.u16 if self._cost_kind == _lib.COST_U16 else self.costs.f64
+
+    def _simulate_fused(self, params: QaoaParams, initial_weight, expectation: bool):
+        """One fq_qaoa_evolve_sharded program: local groups on this shard,
+        the global group as peer-memory passes fused across layers."""
+        n, nl, K = self.n, self.n_local, self.K
+        if nl < 12:
+            raise ValueError(f"global_mode='fused' needs >= 12 qubits per shard (got {nl}); use 'p2p'")
+        psi = self._p2p_shard()
+        if self._cost_peers is None:
+            self._cost_peers = self._map_peers(self._cost_tensor().data_ptr())
+        init = initial_weight is None
+        if not init:
+            psi.copy_(self.initial_state(initial_weight))
+        exp = torch.zeros(1, dtype=torch.float64, device=psi.device) if expectation else None
+        view = DeviceCosts(nl, u16=self.costs.u16, scale=self.costs.scale, offset=self.costs.offset,
+                           levels=self.costs.levels) if self._cost_kind == _lib.COST_U16 else \
+            DeviceCosts(nl, f64=self.costs.f64)
+        evolve_sharded(self._peers, self._cost_peers, view, n, self.k, self.mixer, params, init, rank=self.rank,
+                       flags=self._flag_ptrs, epoch=self._epoch, err_ptr=self._flags.data_ptr() + 4 * K,
+                       expectation_out=exp)
+        # the reference's logical exchange count (Alg. 4: two per X layer)
+        self.exchange_count += 2 * params.p
+        instrumentation.bump("exchange", 2 * params.p)
+        self._state = psi
+        if not expectation:
+            return None
+        self.check_barrier()
+        dist.all_reduce(exp, op=dist.ReduceOp.SUM, group=self.group)
+        return float(exp.item())
 
     def close(self) -> None:
         for ptr, off in self._opened:

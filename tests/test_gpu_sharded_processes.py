@@ -44,12 +44,14 @@ def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange", dev_barrie
         rng = np.random.default_rng(11)
         g, b = rng.uniform(0, 1, p), rng.uniform(0, 1, p)
         poly = labs_terms(n) if kind in ("x", "custom") else portfolio_terms(n)
+        if kind == "xf":  # float64 costs under the X mixer
+            kind = "x"
         sim = ShardedQaoaSimulator(poly, mixer=_mixer(kind, n), chunk_bytes=chunk, global_mode=mode,
                                    device_barrier=dev_barrier)
         E = sim.simulate_qaoa(g, b, initial_weight=n // 2 if kind.startswith("xy") else None)
         ov = sim.overlap()
         q.put((rank, E, ov, sim.exchange_count, sim.shard.cpu().numpy()))
-        if mode == "p2p":
+        if mode in ("p2p", "fused"):
             dist.barrier()
             sim.close()
     finally:
@@ -60,7 +62,9 @@ def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange", dev_barrie
                          [(16, 3, "x", None, "exchange", True), (17, 2, "x", 1 << 16, "exchange", True),
                           (14, 2, "xy-ring", None, "exchange", True), (16, 3, "x", None, "p2p", True),
                           (19, 2, "x", None, "p2p", False), (15, 2, "custom", None, "p2p", True),
-                          (15, 2, "custom", None, "exchange", True)])
+                          (15, 2, "custom", None, "exchange", True),
+                          (16, 3, "x", None, "fused", True), (21, 5, "x", None, "fused", True),
+                          (15, 2, "custom", None, "fused", True), (14, 3, "xf", None, "fused", True)])
 def test_two_process_sharded_matches_single_gpu(n, p, kind, chunk, mode, dev_barrier):
     from oracle import oracle as O
     from paper_2309_04841_b200 import Mixer, QaoaSimulator, hamming_weight_state
@@ -81,6 +85,7 @@ def test_two_process_sharded_matches_single_gpu(n, p, kind, chunk, mode, dev_bar
     rng = np.random.default_rng(11)
     g, b = rng.uniform(0, 1, p), rng.uniform(0, 1, p)
     poly = labs_terms(n) if kind in ("x", "custom") else portfolio_terms(n)
+    kind = "x" if kind == "xf" else kind
     sim = QaoaSimulator(terms=poly, mixer=_mixer(kind, n))
     init = hamming_weight_state(n, n // 2) if kind.startswith("xy") else None
     res = sim.simulate_qaoa(g, b, initial=init)
