@@ -415,7 +415,9 @@ static double plan_cost(const std::vector<PlannedPass> &seq, const std::vector<G
         }
         const int sq = pass_seq(gs[pp.group], pp);
         double pc = pass_cost(sq) * (l2_resident ? 1.0 : run_factor((long long)elem << run_bits_of(gs[pp.group]), seq_heavy(sq)));
-        if (kq > 0 && global_count(gs[pp.group], n, kq) > 0) pc *= kGlobalPassCost;
+        // a spanning pass is NVLink-bound: its DRAM run lengths hide behind the link
+        // (and its round program too: the link time is the same for every program)
+        if (kq > 0 && global_count(gs[pp.group], n, kq) > 0) pc = std::max(pc, kGlobalPassCost);
         c += pc;
     }
     return c;

@@ -89,6 +89,27 @@ def test_pass_planner_counts():
     assert _plan(12, 4) == 1  # resident
 
 
+def _plan_sharded(nl, k, p):
+    import ctypes
+
+    layers = (_lib.FqLayer * p)(*[_lib.FqLayer(0.1, 0.2, 1, 0, nl + k) for _ in range(p)])
+    gp = ctypes.c_int()
+    total = _lib.load().fq_plan_sharded_passes(nl, k, p, layers, ctypes.byref(gp))
+    return total, gp.value
+
+
+def test_sharded_planner_counts():
+    # weak scaling at 2^26 amplitudes per GPU (n = 27..29 on 2..8 GPUs): the same
+    # 3 groups as one GPU, the global qubits inside the group that is a fusion
+    # point every other layer -> 1 + 2p passes of which p/2 span the shards
+    for k in (1, 2, 3):
+        assert _plan_sharded(26, k, 10) == (21, 5)
+    # n = 34 on 8 GPUs (n_local 31): 4 groups -> 1 + 3p passes, 5 spanning
+    assert _plan_sharded(31, 3, 10) == (31, 5)
+    assert _plan_sharded(31, 3, 1) == (4, 1)
+    assert _plan_sharded(11, 1, 2) == (-1, 0)  # shards need >= 12 local qubits
+
+
 # ------------------------------------------------------------------ host mirror of the reference
 def test_term_validation():
     assert Term(1.0, (3, 1)).support == (1, 3)
