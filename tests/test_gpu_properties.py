@@ -57,3 +57,27 @@ def test_xy_conserves_hamming_weight(n, kind, w, seed):
     pop = np.bitwise_count(np.arange(1 << n, dtype=np.uint64))
     assert np.sum(np.abs(res.state[pop != w]) ** 2) < 1e-24
     assert np.sum(np.abs(res.state[pop == w]) ** 2) == pytest.approx(1.0, abs=1e-11)
+
+
+@settings(max_examples=20, deadline=None)
+@given(n=st.integers(13, 17), k=st.integers(1, 3), p=st.integers(0, 4), seed=st.integers(0, 2**31 - 1),
+       integer=st.booleans())
+def test_random_sharded_programs_match_single_gpu(n, k, p, seed, integer):
+    """fq_qaoa_evolve_sharded (in-process, K shard views) == the single-state program."""
+    from paper_2309_04841_b200 import QaoaParams
+    from paper_2309_04841_b200.distributed import simulate_qaoa_distributed
+    from paper_2309_04841_b200.qaoa import simulate_qaoa
+
+    if n - k < 12:
+        k = n - 12
+    rng = np.random.default_rng(seed)
+    poly = TermPolynomial.from_pairs(n, random_pairs(rng, n, max_terms=3 * n, integer=integer))
+    g = rng.uniform(-2, 2, p)
+    if p and rng.random() < 0.3:
+        g[rng.integers(0, p)] = 0.0
+    params = QaoaParams(tuple(g), tuple(rng.uniform(-2, 2, p)))
+    init = random_state(rng, n) if rng.random() < 0.3 else None
+    single = simulate_qaoa(poly, params, initial=init)
+    res = simulate_qaoa_distributed(poly, params, 1 << k, initial=init)
+    np.testing.assert_allclose(res.statevector(), single.state, rtol=0, atol=1e-12)
+    assert res.expectation() == pytest.approx(float(single._expectation_dev.item()), rel=1e-10, abs=1e-10)
