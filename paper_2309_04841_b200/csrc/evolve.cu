@@ -424,8 +424,8 @@ static double plan_cost(const std::vector<PlannedPass> &seq, const std::vector<G
 }
 
 // elem: bytes per amplitude (16 complex128, 8 complex64); kq: global qubits of a sharded state
-static std::vector<PlannedPass> plan_x(int n, int nl, const fq_layer *layers, std::vector<Group> &groups, bool fuse,
-                                       int elem, int kq = 0) {
+static std::vector<PlannedPass> plan_x_search(int n, int nl, const fq_layer *layers, std::vector<Group> &groups,
+                                              bool fuse, int elem, int kq) {
     if (g_plan >= 0) {
         auto seq = plan_with(n, nl, layers, groups, g_plan, g_plan == 0 ? 10 : 8, fuse);
         if (plan_cost(seq, groups, n, elem, kq) < 1e299) return seq;  // else: search
@@ -445,6 +445,44 @@ static std::vector<PlannedPass> plan_x(int n, int nl, const fq_layer *layers, st
         }
     }
     return best;
+}
+
+// The search prices 18 candidate plans (~0.1 ms of host time), on the path of
+// every simulate_qaoa call, before the first launch: plans are memoised by
+// everything they depend on (sizes, options, and per layer the qubit range and
+// whether a phase is applied — not the angles).
+struct PlanMemo {
+    std::vector<long long> key;
+    std::vector<PlannedPass> seq;
+    std::vector<Group> groups;
+};
+
+static std::vector<PlannedPass> plan_x(int n, int nl, const fq_layer *layers, std::vector<Group> &groups, bool fuse,
+                                       int elem, int kq = 0) {
+    static std::mutex mu;
+    static std::vector<PlanMemo> memo;
+    static size_t next = 0;
+    std::vector<long long> key = {n, nl, elem, kq, fuse ? 1 : 0, g_plan};
+    key.reserve(key.size() + 3 * (size_t)nl);
+    for (int l = 0; l < nl; ++l) {
+        key.push_back(layers[l].q_lo);
+        key.push_back(layers[l].q_hi);
+        key.push_back(phase_active(layers[l]) ? 1 : 0);
+    }
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        for (auto &m : memo)
+            if (m.key == key) {
+                groups = m.groups;
+                return m.seq;
+            }
+    }
+    auto seq = plan_x_search(n, nl, layers, groups, fuse, elem, kq);
+    std::lock_guard<std::mutex> lock(mu);
+    PlanMemo m{std::move(key), seq, groups};
+    if (memo.size() < 32) memo.push_back(std::move(m));
+    else memo[next++ % 32] = std::move(m);
+    return seq;
 }
 
 // pdep: the bits of x into the positions NOT set in mask (ascending)
