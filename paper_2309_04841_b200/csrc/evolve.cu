@@ -819,6 +819,8 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
 int plan_xy_passes(int n, int mixer, const std::vector<std::pair<int, int>> &gates, int *rounds);
 static int g_xy_tiled = 1;   // tiled XY passes (0: one pair kernel per gate, the reference's structure)
 extern int g_xy_min_run;     // xy.cu
+extern int g_xy_row_cap;     // xy.cu
+extern int g_xy_pad;         // xy.cu
 
 static int run_xy_program(const fq_evolve_desc *d, cudaStream_t st) {
     const int n = d->n;
@@ -1025,6 +1027,8 @@ int fq_set_option(const char *name, int value) {
         {"xy_tiled", &g_xy_tiled, 0, 1},    // tiled XY passes (0: one kernel per gate)
         {"zigzag", &g_zigzag, 0, 1},        // alternate tile walk direction pass to pass
         {"xy_min_run", &g_xy_min_run, 0, 8},  // XY pass tiles: min contiguous run, log2 amplitudes (0 = auto)
+        {"xy_row_cap", &g_xy_row_cap, 0, 64},  // XY pass cut: new qubits per leading qubit (0 = auto)
+        {"xy_pad", &g_xy_pad, 0, 1},        // XY passes: gate-free load / store rounds for coalescing
         {"probe", &g_probe, 0, 7},          // development: isolate phase costs (results invalid when != 0)
     };
     for (auto &o : opts) {

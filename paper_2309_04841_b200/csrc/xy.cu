@@ -22,7 +22,8 @@
 namespace fq {
 
 constexpr int kXyMaxRounds = 24;
-int g_xy_min_run = 0;  // minimum contiguous run (log2 amplitudes) of an XY pass tile; 0 = per mixer (measured)
+int g_xy_pad = 1;      // option xy_pad: gate-free first / last rounds keep loads and stores on tile bits 0..4
+int g_xy_min_run = 0;  // minimum contiguous run (log2 amplitudes) of an XY pass tile; 0 = chosen by the cost model
 constexpr int kXyMaxGates = 6;  // C(4, 2): distinct pairs of one 4-bit register set
 
 struct XyRound {
@@ -236,22 +237,30 @@ static std::vector<int> tile_for(int n, const std::vector<int> &targets) {
 // gates in order; a gate joins the current group if none of its qubits was
 // touched by a gate left behind (it would have to wait for it) and its qubits
 // fit the capacity test; a gate left behind blocks its qubits.
+// row_cap: a gate's leading (first) qubit may bring at most row_cap new other
+// qubits into a group — so a pass over the complete graph's lexicographic
+// order takes a block of rows x columns instead of one long row.
 template <typename Fits>
 static std::vector<std::vector<int>> cut_groups(const std::vector<std::pair<int, int>> &gates, std::vector<int> idx,
-                                                Fits fits) {
+                                                Fits fits, int row_cap = 64) {
     std::vector<std::vector<int>> groups;
     while (!idx.empty()) {
         std::vector<int> taken, rest, qubits;
         std::vector<char> blocked(64, 0);
+        std::vector<int> row_new(64, 0);
         for (int gi : idx) {
             const int a = gates[gi].first, b = gates[gi].second;
             bool ok = !blocked[a] && !blocked[b];
             if (ok) {
                 std::vector<int> q2 = qubits;
+                const bool new_b = std::find(q2.begin(), q2.end(), b) == q2.end();
                 if (std::find(q2.begin(), q2.end(), a) == q2.end()) q2.push_back(a);
-                if (std::find(q2.begin(), q2.end(), b) == q2.end()) q2.push_back(b);
-                ok = fits(q2);
-                if (ok) qubits = q2;
+                if (new_b) q2.push_back(b);
+                ok = fits(q2) && (!new_b || row_new[a] < row_cap);
+                if (ok) {
+                    qubits = q2;
+                    row_new[a] += new_b ? 1 : 0;
+                }
             }
             if (ok) {
                 taken.push_back(gi);
@@ -323,14 +332,8 @@ static std::vector<std::vector<int>> round_cut(const std::vector<std::pair<int, 
     return rounds;
 }
 
-// B200, portfolio n = 26: 64-B runs are the best trade for the ring's few
-// passes, 512-B runs for the complete graph's many (scripts/bench_configs.py, FQ_OPTS)
-static int xy_min_run(int mixer) {
-    if (g_xy_min_run > 0) return g_xy_min_run;
-    return mixer == FQ_MIXER_XY_RING ? 3 : 5;
-}
-
-static std::vector<XyPassPlan> plan_xy(int n, const std::vector<std::pair<int, int>> &gates, int min_run) {
+static std::vector<XyPassPlan> plan_xy_with(int n, const std::vector<std::pair<int, int>> &gates, int min_run,
+                                            int row_cap) {
     std::vector<int> all(gates.size());
     for (size_t i = 0; i < gates.size(); ++i) all[i] = (int)i;
     // passes: the tile (targets + spectators) must keep runs of >= 16 amplitudes
@@ -338,7 +341,7 @@ static std::vector<XyPassPlan> plan_xy(int n, const std::vector<std::pair<int, i
         return (int)q.size() <= kTileBits && run_bits_of(tile_for(n, q)) >= min_run;
     };
     std::vector<XyPassPlan> plans;
-    for (auto &pg : cut_groups(gates, all, pass_fits)) {
+    for (auto &pg : cut_groups(gates, all, pass_fits, row_cap)) {
         XyPassPlan pl;
         std::vector<int> q;
         for (int gi : pg) {
@@ -370,11 +373,11 @@ static std::vector<XyPassPlan> plan_xy(int n, const std::vector<std::pair<int, i
             return true;
         };
         const std::vector<int> top = {8, 9, 10, 11};
-        if (!low_ok(pl.round_bits.front())) {
+        if (g_xy_pad && !low_ok(pl.round_bits.front())) {
             pl.round_bits.insert(pl.round_bits.begin(), top);
             pl.round_gates.insert(pl.round_gates.begin(), std::vector<std::pair<int, int>>());
         }
-        if (!low_ok(pl.round_bits.back())) {
+        if (g_xy_pad && !low_ok(pl.round_bits.back())) {
             pl.round_bits.push_back(top);
             pl.round_gates.push_back({});
         }
@@ -390,11 +393,11 @@ static std::vector<XyPassPlan> plan_xy(int n, const std::vector<std::pair<int, i
             const size_t r1 = std::min(pl.round_bits.size(), r0 + kChunk);
             part.round_bits.assign(pl.round_bits.begin() + r0, pl.round_bits.begin() + r1);
             part.round_gates.assign(pl.round_gates.begin() + r0, pl.round_gates.begin() + r1);
-            if (!low_ok(part.round_bits.front())) {
+            if (g_xy_pad && !low_ok(part.round_bits.front())) {
                 part.round_bits.insert(part.round_bits.begin(), top);
                 part.round_gates.insert(part.round_gates.begin(), std::vector<std::pair<int, int>>());
             }
-            if (!low_ok(part.round_bits.back())) {
+            if (g_xy_pad && !low_ok(part.round_bits.back())) {
                 part.round_bits.push_back(top);
                 part.round_gates.push_back({});
             }
@@ -402,6 +405,52 @@ static std::vector<XyPassPlan> plan_xy(int n, const std::vector<std::pair<int, i
         }
     }
     return plans;
+}
+
+int g_xy_row_cap = 0;  // option xy_row_cap: 0 = chosen by the cost model
+
+// Relative cost of one register round (a shared-memory transpose of the whole
+// state plus its gates) against one HBM pass of the tile kernel (B200).
+// Fitted on B200 (portfolio n = 26, XY complete, 7 plans): 0.30 ms per pass,
+// 0.056 ms per round.
+constexpr double kXyRoundCost = 0.19;
+
+// Plans for every (minimum run, row cap) and the cheapest by
+// passes + kXyRoundCost * rounds; memoised per (n, gate list, options).
+static std::vector<XyPassPlan> plan_xy(int n, const std::vector<std::pair<int, int>> &gates, int mixer) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::vector<int>, std::vector<XyPassPlan>>> memo;
+    std::vector<int> key = {n, mixer, g_xy_min_run, g_xy_row_cap, g_xy_pad, (int)gates.size()};
+    for (auto &gp : gates) {
+        key.push_back(gp.first);
+        key.push_back(gp.second);
+    }
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        for (auto &m : memo)
+            if (m.first == key) return m.second;
+    }
+    std::vector<int> runs = g_xy_min_run > 0 ? std::vector<int>{g_xy_min_run} : std::vector<int>{3, 4, 5};
+    std::vector<int> caps = g_xy_row_cap > 0 ? std::vector<int>{g_xy_row_cap} : std::vector<int>{1, 2, 3, 4, 6, 64};
+    std::vector<XyPassPlan> best;
+    double best_cost = 1e300;
+    for (int mr : runs)
+        for (int cap : caps) {
+            auto plans = plan_xy_with(n, gates, mr, cap);
+            size_t rounds = 0;
+            for (auto &pl : plans) rounds += pl.round_bits.size();
+            // shorter runs cost DRAM efficiency (as the X passes, evolve.cu run_factor)
+            const double run_pen = mr >= 5 ? 1.0 : mr == 4 ? 1.04 : 1.18;
+            const double c = run_pen * (double)plans.size() + kXyRoundCost * (double)rounds;
+            if (c < best_cost - 1e-9) {
+                best_cost = c;
+                best = std::move(plans);
+            }
+        }
+    std::lock_guard<std::mutex> lock(mu);
+    if (memo.size() >= 16) memo.erase(memo.begin());
+    memo.emplace_back(key, best);
+    return best;
 }
 
 static void fill_round(XyRound &R, const std::vector<int> &bits, const std::vector<std::pair<int, int>> &gl,
@@ -473,7 +522,7 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
     const int n = d->n;
     const long long size = 1LL << n;
     double2 *psi = static_cast<double2 *>(d->psi);
-    const auto plans = plan_xy(n, gates, xy_min_run(d->mixer));
+    const auto plans = plan_xy(n, gates, d->mixer);
     for (auto &pl : plans)
         if ((int)pl.round_bits.size() > kXyMaxRounds) {
             set_error("run_xy_tiled: a pass needs %d register rounds (max %d)", (int)pl.round_bits.size(),
@@ -560,7 +609,7 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
 }
 
 int plan_xy_passes(int n, int mixer, const std::vector<std::pair<int, int>> &gates, int *rounds) {
-    const auto plans = plan_xy(n, gates, xy_min_run(mixer));
+    const auto plans = plan_xy(n, gates, mixer);
     if (rounds) {
         *rounds = 0;
         for (auto &pl : plans) *rounds += (int)pl.round_bits.size();
