@@ -223,7 +223,10 @@ def test_rebase_u16():
 
     rng = np.random.default_rng(5)
     for size in (8, 4096 + 5, 1 << 16):
-        lv = rng.integers(300, 65535, size).astype(np.uint16)
+        lv = rng.integers(300, 65335, size).astype(np.uint16)
         t = torch.from_numpy(lv.view(np.int16)).cuda().view(torch.uint16)
         _lib.call("fq_rebase_u16", t.data_ptr(), size, 300, _lib.stream())
         np.testing.assert_array_equal(t.view(torch.int16).cpu().numpy().view(np.uint16), lv - 300)
+        # negative delta: levels move up (the sharded common origin)
+        _lib.call("fq_rebase_u16", t.data_ptr(), size, -200, _lib.stream())
+        np.testing.assert_array_equal(t.view(torch.int16).cpu().numpy().view(np.uint16), lv - 100)
