@@ -11,4 +11,10 @@ timeout 300 python scripts/bench_pass.py --opts "plan=-1" --detail > gpurun_out/
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch_$TAG.log 2>&1
 timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:k_pass -s 63 -c 21 --csv --log-file gpurun_out/traffic_$TAG.csv python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_traffic_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pass -s 63 -c 4 -o gpurun_out/prof_$TAG python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_full_$TAG.log 2>&1
+# extra kernels: complex64 passes, the spanning (sharded, G) pass in-process, the XY pass; all BASELINE configs
+timeout 600 python bench.py --state c64 --steps 20 --warmup 5 > gpurun_out/bench_c64_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_pass16<.*float' -s 20 -c 3 -o gpurun_out/prof_c64_$TAG python bench.py --state c64 --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_c64_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_pass16<.*bool.1>' -c 2 -o gpurun_out/prof_g_$TAG python scripts/bench_sharded_inprocess.py --n 26 --steps 1 > gpurun_out/ncu_g_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_xy_pass -s 17 -c 2 -o gpurun_out/prof_xy_$TAG python scripts/bench_configs.py --only 4 --skip-cpu > gpurun_out/ncu_xy_$TAG.log 2>&1
+timeout 1500 python scripts/bench_configs.py > gpurun_out/configs_$TAG.jsonl 2> gpurun_out/configs_$TAG.err
 echo done
