@@ -244,7 +244,10 @@ typedef struct fq_shard_desc {
  * below); layer qubit ranges and the custom su2 table use global positions
  * [0, n); desc->init_amp = 2^(-n/2); desc->expectation_dev receives this
  * rank's partial sum (rank >= 0: all-reduce it) or the total (rank = -1).
- * complex128, X and custom mixers, n_local >= 12. */
+ * XY mixers: the tiled XY plan over all n qubits; a pass whose tile holds
+ * global qubits spans the shards it covers, each rank taking the tiles of its
+ * own shard set (replaces the reference's park-and-exchange per global pair,
+ * distributed.py:160-207).  complex128, n_local >= 12. */
 int fq_qaoa_evolve_sharded(const fq_evolve_desc *desc, const fq_shard_desc *shards, void *stream);
 
 /* Pass count of fq_qaoa_evolve_sharded's plan and, in *global_passes, how many

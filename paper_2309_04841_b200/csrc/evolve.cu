@@ -530,17 +530,6 @@ static int launch_pass(int mix, int cost, bool c64, const PassParams &P, const P
                           : launch_pass_rx_f64_light(P, M, seq, ph, ma, mb, k, grid, st);
 }
 
-// Sharded execution context (fq_qaoa_evolve_sharded); null for one state.
-struct ShardCtx {
-    int k = 0, K = 1;
-    int rank = 0;                          // -1: every shard belongs to this process (one stream)
-    void *const *shards = nullptr;         // [K] state shards as mapped in this process
-    const void *const *costs = nullptr;    // [K] cost shards
-    void *const *flags = nullptr;          // [K] peer barrier flag arrays (rank >= 0)
-    unsigned *epoch = nullptr;
-    int *err = nullptr;
-};
-
 static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCtx *sh = nullptr) {
     const int nl = d->n;                      // qubits per shard (= n for one state)
     const int kq = sh ? sh->k : 0;
@@ -815,7 +804,7 @@ static void xy_gates(int n, int kind, std::vector<std::pair<int, int>> &g) {
 }
 
 int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>> &gates, cudaStream_t st,
-                 int *passes_out);
+                 int *passes_out, const ShardCtx *sh = nullptr);
 int plan_xy_passes(int n, int mixer, const std::vector<std::pair<int, int>> &gates, int *rounds);
 static int g_xy_tiled = 1;   // tiled XY passes (0: one pair kernel per gate, the reference's structure)
 extern int g_xy_min_run;     // xy.cu
@@ -980,8 +969,7 @@ int fq_qaoa_evolve_sharded(const fq_evolve_desc *d, const fq_shard_desc *s, void
     FQ_CHECK_ARG(d->n >= kTileBits && d->n + s->k <= 40, "fq_qaoa_evolve_sharded: n_local=%d must be >= %d", d->n,
                  kTileBits);
     FQ_CHECK_ARG(d->state_kind == FQ_STATE_C128, "fq_qaoa_evolve_sharded: complex128 states only");
-    FQ_CHECK_ARG(d->mixer == FQ_MIXER_X || d->mixer == FQ_MIXER_CUSTOM,
-                 "fq_qaoa_evolve_sharded: X or custom mixers (XY mixers use the exchange path)");
+    FQ_CHECK_ARG(d->mixer >= FQ_MIXER_X && d->mixer <= FQ_MIXER_CUSTOM, "fq_qaoa_evolve_sharded: bad mixer");
     FQ_CHECK_ARG(d->mixer != FQ_MIXER_CUSTOM || d->su2, "fq_qaoa_evolve_sharded: custom mixer needs su2 table");
     FQ_CHECK_ARG(d->n_layers >= 0 && (d->n_layers == 0 || d->layers), "fq_qaoa_evolve_sharded: bad layers");
     FQ_CHECK_ARG(d->cost_kind == FQ_COST_F64 || d->cost_kind == FQ_COST_U16, "fq_qaoa_evolve_sharded: bad cost kind");
@@ -1000,6 +988,11 @@ int fq_qaoa_evolve_sharded(const fq_evolve_desc *d, const fq_shard_desc *s, void
     ctx.flags = s->flags;
     ctx.epoch = s->epoch;
     ctx.err = s->barrier_err;
+    if (d->mixer == FQ_MIXER_XY_RING || d->mixer == FQ_MIXER_XY_COMPLETE) {
+        std::vector<std::pair<int, int>> gates;
+        xy_gates(d->n + s->k, d->mixer, gates);
+        return run_xy_tiled(d, gates, static_cast<cudaStream_t>(stream), nullptr, &ctx);
+    }
     return run_x_program(d, static_cast<cudaStream_t>(stream), &ctx);
 }
 

@@ -540,6 +540,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
     }
 }
 
+// Sharded execution context (fq_qaoa_evolve_sharded); null for one state.
+struct ShardCtx {
+    int k = 0, K = 1;
+    int rank = 0;                          // -1: every shard belongs to this process (one stream)
+    void *const *shards = nullptr;         // [K] state shards as mapped in this process
+    const void *const *costs = nullptr;    // [K] cost shards
+    void *const *flags = nullptr;          // [K] peer barrier flag arrays (rank >= 0)
+    unsigned *epoch = nullptr;
+    int *err = nullptr;
+};
+
 // ---------------------------------------------------------------- launch
 struct PassMaps {
     alignas(64) CUtensorMap state;

@@ -51,7 +51,25 @@ struct XyParams {
     int cm_rank, cm_shift[5], cm_bits[5];     // cost map (cm_rank = 0: not needed)
     int nrounds;
     XyRound rounds[kXyMaxRounds];
+    // sharded state (G = true): amplitude indices are global; index k lives in
+    // shard k >> nl at local offset k & (2^nl - 1) (peer-mapped shard pointers)
+    long long tile0;  // first tile of this launch
+    int nl;
+    double2 *shard[8];
+    const void *cshard[8];
 };
+
+template <bool G>
+__device__ __forceinline__ double2 *xy_amp(const XyParams &P, long long k) {
+    if constexpr (G) return P.shard[k >> P.nl] + (k & ((1LL << P.nl) - 1));
+    else return P.psi + k;
+}
+
+template <bool G, typename C>
+__device__ __forceinline__ const C *xy_cost(const XyParams &P, long long k) {
+    if constexpr (G) return static_cast<const C *>(P.cshard[k >> P.nl]) + (k & ((1LL << P.nl) - 1));
+    else return static_cast<const C *>(P.costs) + k;
+}
 
 // XOR swizzle of a 12-bit tile index (bijective; GF(2)-linear, so the slot of
 // thread part | register part is the XOR of the parts' slots).  The bank group
@@ -129,7 +147,7 @@ __device__ __forceinline__ double2 xy_phase(const XyParams &P, CostRaw<COST> raw
     }
 }
 
-template <int COST, int PH>
+template <int COST, int PH, bool G = false>
 __global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__ XyParams P,
                                                          const __grid_constant__ CUtensorMap tm_state,
                                                          const __grid_constant__ CUtensorMap tm_cost) {
@@ -147,8 +165,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__
     const long long thr_last = xy_tphys(P, P.rounds[P.nrounds - 1], tid);
     double eacc = 0.0;
     for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
-        const long long base = xy_tile_base(P.tile_pos, t);
-        if (P.pf && tid == 0 && t + gridDim.x < P.n_tiles) {  // next tile of this CTA into L2
+        const long long base = xy_tile_base(P.tile_pos, P.tile0 + t);
+        if (!G && P.pf && tid == 0 && t + gridDim.x < P.n_tiles) {  // next tile of this CTA into L2
             int c[5];
             if (!P.init && P.sm_rank) {
                 tile_coords(t + gridDim.x, P.sm_rank, P.sm_shift, P.sm_bits, c);
@@ -165,15 +183,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__
             for (int i = 0; i < kRegs; ++i) v[i] = make_double2(P.init_amp, 0.0);
         } else {
 #pragma unroll
-            for (int i = 0; i < kRegs; ++i) v[i] = ld_stream(P.psi + base + thr_first + P.roff_first[i]);
+            for (int i = 0; i < kRegs; ++i) v[i] = ld_stream(xy_amp<G>(P, base + thr_first + P.roff_first[i]));
         }
         if (PH) {
             CostRaw<COST> raw[kRegs];
 #pragma unroll
             for (int i = 0; i < kRegs; ++i) {
                 const long long k = base + thr_first + P.roff_first[i];
-                if constexpr (COST == FQ_COST_F64) raw[i] = static_cast<const double *>(P.costs)[k];
-                else raw[i] = static_cast<const unsigned short *>(P.costs)[k];
+                if constexpr (COST == FQ_COST_F64) raw[i] = *xy_cost<G, double>(P, k);
+                else raw[i] = *xy_cost<G, unsigned short>(P, k);
             }
 #pragma unroll
             for (int i = 0; i < kRegs; ++i)
@@ -199,11 +217,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__
             const long long k = base + thr_last + P.roff_last[i];
             if (P.expect) {
                 double cv;
-                if constexpr (COST == FQ_COST_F64) cv = static_cast<const double *>(P.costs)[k];
-                else cv = decode_u16(static_cast<const unsigned short *>(P.costs)[k], P.cost_scale, P.cost_offset);
+                if constexpr (COST == FQ_COST_F64) cv = *xy_cost<G, double>(P, k);
+                else cv = decode_u16(*xy_cost<G, unsigned short>(P, k), P.cost_scale, P.cost_offset);
                 eacc += cv * (v[i].x * v[i].x + v[i].y * v[i].y);
             }
-            st_stream(P.psi + k, v[i]);
+            st_stream(xy_amp<G>(P, k), v[i]);
         }
     }
     if (P.expect) {
@@ -501,28 +519,34 @@ struct XyMaps {
     alignas(64) CUtensorMap cost;
 };
 
-template <int COST, int PH>
+template <int COST, int PH, bool G = false>
 static int launch_xy(const XyParams &P, const XyMaps &M, int grid, cudaStream_t st) {
     static bool configured = false;
     const size_t smem = (size_t)(kTile + (kTableLo + kMaxTableHi) * kCopies) * sizeof(double2);
     if (!configured) {
-        cudaFuncSetAttribute(k_xy_pass<COST, PH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_xy_pass<COST, PH, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
     const size_t need = (size_t)(kTile + (PH && COST == FQ_COST_U16 ? (kTableLo + P.table_hi) * kCopies : 0)) *
                         sizeof(double2);
-    k_xy_pass<COST, PH><<<grid, kThreads, need, st>>>(P, M.state, M.cost);
+    k_xy_pass<COST, PH, G><<<grid, kThreads, need, st>>>(P, M.state, M.cost);
     FQ_LAUNCHED("k_xy_pass");
     return FQ_OK;
 }
 
 // Whole XY program (n >= 13): p x (phase, gate sequence), expectation.
+// Sharded (sh != null, fq_qaoa_evolve_sharded): the plan covers all n = nl + k
+// qubits; a pass whose tile holds global qubits spans the shards it covers
+// (G kernel, shard pointer per amplitude index), each rank taking the tiles of
+// its own shard set, with device barriers around it; other passes run on the
+// rank's own shard(s).
 int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>> &gates, cudaStream_t st,
-                 int *passes_out) {
-    const int n = d->n;
-    const long long size = 1LL << n;
-    double2 *psi = static_cast<double2 *>(d->psi);
-    const auto plans = plan_xy(n, gates, d->mixer);
+                 int *passes_out, const ShardCtx *sh) {
+    const int nl = d->n;
+    const int kq = sh ? sh->k : 0;
+    const int nv = nl + kq, K = 1 << kq;
+    const long long size = 1LL << nl;
+    const auto plans = plan_xy(nv, gates, d->mixer);
     for (auto &pl : plans)
         if ((int)pl.round_bits.size() > kXyMaxRounds) {
             set_error("run_xy_tiled: a pass needs %d register rounds (max %d)", (int)pl.round_bits.size(),
@@ -535,18 +559,34 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
         const int rows = ((d->cost_levels - 1) >> 6) + 1;
         table_hi = rows <= kMaxTableHi ? rows : 0;
     }
+    std::vector<int> mine;
+    if (!sh) mine.push_back(0);
+    else if (sh->rank >= 0) mine.push_back(sh->rank);
+    else for (int r = 0; r < K; ++r) mine.push_back(r);
+    auto shard_psi = [&](int r) { return static_cast<double2 *>(sh ? sh->shards[r] : d->psi); };
+    auto shard_costs = [&](int r) { return sh ? sh->costs[r] : d->costs; };
+    auto barrier = [&]() -> int {
+        if (!sh || sh->rank < 0) return FQ_OK;
+        return fq_peer_barrier(sh->flags, K, sh->rank, ++*sh->epoch, sh->err, st);
+    };
     const int sms = sm_count() > 0 ? sm_count() : 148;
-    const long long n_tiles = 1LL << (n - kTileBits);
+    const long long n_tiles = 1LL << (nl - kTileBits);
     const int grid = (int)std::min<long long>(n_tiles, (long long)sms * 2);
     bool init_pending = d->init != 0;
+    double *const shard_sums = d->scratch ? d->scratch + FQ_SCRATCH_DOUBLES - 16 : nullptr;
     XyParams *P = new XyParams;
+    auto fail = [&](int s) {
+        delete P;
+        return s;
+    };
     for (int l = 0; l < d->n_layers; ++l) {
         const fq_layer &L = d->layers[l];
         for (size_t pi = 0; pi < plans.size(); ++pi) {
             const XyPassPlan &pl = plans[pi];
+            int gmask = 0;  // global qubits among the tile bits
+            for (int i = 0; i < kTileBits; ++i)
+                if (pl.tile[i] >= nl) gmask |= 1 << (pl.tile[i] - nl);
             std::memset(P, 0, sizeof *P);
-            P->psi = psi;
-            P->costs = d->costs;
             P->cost_scale = d->cost_scale;
             P->cost_offset = d->cost_offset;
             P->partials = d->scratch;
@@ -554,7 +594,6 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
             P->gamma = L.gamma;
             P->c = std::cos(L.beta);
             P->s = std::sin(L.beta);
-            P->n_tiles = n_tiles;
             for (int i = 0; i < kTileBits; ++i) P->tile_pos[i] = pl.tile[i];
             P->init = init_pending ? 1 : 0;
             init_pending = false;
@@ -573,38 +612,94 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
                 P->roff_last[i] = b;
             }
             const bool ph = pi == 0 && L.apply_phase && L.gamma != 0.0;
-            XyMaps M;
-            std::memset(&M, 0, sizeof M);
-            P->pf = 1;
-            P->sm_rank = cached_tile_map(&M.state, psi, n, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2,
-                                        P->sm_shift, P->sm_bits);
-            if (ph || P->expect)
-                P->cm_rank = d->cost_kind == FQ_COST_F64
-                                 ? cached_tile_map(&M.cost, d->costs, n, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
-                                                  1, P->cm_shift, P->cm_bits)
-                                 : cached_tile_map(&M.cost, d->costs, n, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
-                                                  1, P->cm_shift, P->cm_bits);
-            int s;
-            if (d->cost_kind == FQ_COST_U16) s = ph ? launch_xy<FQ_COST_U16, 1>(*P, M, grid, st) : launch_xy<FQ_COST_U16, 0>(*P, M, grid, st);
-            else s = ph ? launch_xy<FQ_COST_F64, 1>(*P, M, grid, st) : launch_xy<FQ_COST_F64, 0>(*P, M, grid, st);
-            if (s) {
-                delete P;
-                return s;
+            int launches = 0;
+            if (gmask) {
+                // spanning pass: tile index = [non-tile global bits | local non-tile bits]; the
+                // 2^(k - kt) shard sets are contiguous tile ranges, split among their members
+                if (int s = barrier()) return fail(s);
+                const long long T = 1LL << (nv - kTileBits);
+                P->nl = nl;
+                for (int r = 0; r < K; ++r) {
+                    P->shard[r] = static_cast<double2 *>(sh->shards[r]);
+                    P->cshard[r] = sh->costs[r];
+                }
+                P->psi = P->shard[0];
+                P->costs = P->cshard[0];
+                P->pf = 0;
+                if (sh->rank < 0) {
+                    P->tile0 = 0;
+                    P->n_tiles = T;
+                } else {
+                    int g_nt = 0, g_t = 0, cnt_nt = 0, cnt_t = 0;
+                    for (int b = 0; b < kq; ++b) {
+                        const int bit = (sh->rank >> b) & 1;
+                        if ((gmask >> b) & 1) g_t |= bit << cnt_t++;
+                        else g_nt |= bit << cnt_nt++;
+                    }
+                    const long long Tset = T >> cnt_nt;  // tiles of one shard set
+                    P->n_tiles = Tset >> cnt_t;
+                    P->tile0 = (long long)g_nt * Tset + (long long)g_t * P->n_tiles;
+                }
+                XyMaps M;
+                std::memset(&M, 0, sizeof M);
+                const int ggrid = (int)std::min<long long>(P->n_tiles, (long long)sms * 2);
+                int s;
+                if (d->cost_kind == FQ_COST_U16)
+                    s = ph ? launch_xy<FQ_COST_U16, 1, true>(*P, M, ggrid, st) : launch_xy<FQ_COST_U16, 0, true>(*P, M, ggrid, st);
+                else
+                    s = ph ? launch_xy<FQ_COST_F64, 1, true>(*P, M, ggrid, st) : launch_xy<FQ_COST_F64, 0, true>(*P, M, ggrid, st);
+                if (s) return fail(s);
+                launches = ggrid;
+                if (int s2 = barrier()) return fail(s2);
+            } else {
+                P->n_tiles = n_tiles;
+                for (int r : mine) {
+                    P->psi = shard_psi(r);
+                    P->costs = shard_costs(r);
+                    P->partials = d->scratch + launches;
+                    XyMaps M;
+                    std::memset(&M, 0, sizeof M);
+                    P->pf = 1;
+                    P->sm_rank = cached_tile_map(&M.state, P->psi, nl, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2,
+                                                P->sm_shift, P->sm_bits);
+                    P->cm_rank = 0;
+                    if (ph || P->expect)
+                        P->cm_rank = d->cost_kind == FQ_COST_F64
+                                         ? cached_tile_map(&M.cost, P->costs, nl, P->tile_pos,
+                                                          CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 1, P->cm_shift, P->cm_bits)
+                                         : cached_tile_map(&M.cost, P->costs, nl, P->tile_pos,
+                                                          CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, 1, P->cm_shift, P->cm_bits);
+                    int s;
+                    if (d->cost_kind == FQ_COST_U16)
+                        s = ph ? launch_xy<FQ_COST_U16, 1>(*P, M, grid, st) : launch_xy<FQ_COST_U16, 0>(*P, M, grid, st);
+                    else
+                        s = ph ? launch_xy<FQ_COST_F64, 1>(*P, M, grid, st) : launch_xy<FQ_COST_F64, 0>(*P, M, grid, st);
+                    if (s) return fail(s);
+                    launches += grid;
+                }
             }
             if (P->expect) {
-                k_sum_partials<<<1, 32, 0, st>>>(d->scratch, grid, d->expectation_dev);
+                k_sum_partials<<<1, 32, 0, st>>>(d->scratch, launches, d->expectation_dev);
                 FQ_LAUNCHED("k_sum_partials");
             }
         }
     }
     delete P;
     if (init_pending) {  // zero layers
-        int s = fq_init_state(psi, size, -1, d->init_amp, 0, st);
-        if (s) return s;
+        for (int r : mine)
+            if (int s = fq_init_state(shard_psi(r), size, -1, d->init_amp, 0, st)) return s;
     }
-    if (d->n_layers == 0 && d->expectation_dev)
-        return fq_expectation(psi, d->costs, d->cost_kind, d->cost_scale, d->cost_offset, size, d->expectation_dev,
-                              d->scratch, st);
+    if (d->n_layers == 0 && d->expectation_dev) {
+        if (mine.size() == 1)
+            return fq_expectation(shard_psi(mine[0]), shard_costs(mine[0]), d->cost_kind, d->cost_scale, d->cost_offset,
+                                  size, d->expectation_dev, d->scratch, st);
+        for (size_t i = 0; i < mine.size(); ++i)
+            if (int s = fq_expectation(shard_psi(mine[i]), shard_costs(mine[i]), d->cost_kind, d->cost_scale,
+                                       d->cost_offset, size, shard_sums + i, d->scratch, st))
+                return s;
+        k_sum_partials<<<1, 32, 0, st>>>(shard_sums, (int)mine.size(), d->expectation_dev);
+        FQ_LAUNCHED("k_sum_partials");
+    }
     return FQ_OK;
 }
 

@@ -291,6 +291,16 @@ def global_su2_pass(shard_ptrs: Sequence[int], k: int, shard_size: int, part: in
     _lib.call("fq_global_su2_pass", ptrs, k, shard_size, part, parts, coef.ctypes.data, _lib.stream())
 
 
+def _logical_exchanges(mixer: Mixer, n: int, k: int, p: int) -> int:
+    """The reference's exchange count for p layers (API contract): Alg. 4's two
+    per X / custom layer, two per gate touching a global qubit for XY mixers
+    (distributed.py:160-207)."""
+    if mixer.kind in ("x", "custom"):
+        return 2 * p
+    edges = ring_edges(n) if mixer.kind == "xy-ring" else complete_edges(n)
+    return 2 * p * sum(1 for i, j in edges if max(i, j) >= n - k)
+
+
 def evolve_sharded(shard_ptrs: Sequence[int], cost_ptrs: Sequence[int], costs: DeviceCosts, n: int, k: int,
                    mixer: Mixer, params: QaoaParams, init: bool, rank: int = -1, flags=None, epoch=None,
                    err_ptr: int | None = None, expectation_out: torch.Tensor | None = None) -> None:
@@ -353,14 +363,15 @@ def simulate_qaoa_distributed(problem, params: QaoaParams, K: int, mixer: "str |
     sharded = ShardedState(n, k, list(state.view(K, -1).unbind(0)))
     sc = ShardedCosts(n, k, _slice_device_costs(dc, K))
     n_local = n - k
-    if fused and 1 <= k <= 3 and n_local >= 12 and mixer.kind in ("x", "custom"):
+    if fused and 1 <= k <= 3 and n_local >= 12:
         # one sharded program: the global group's passes span the K shard views
         # (the same kernels a multi-GPU rank runs over peer memory)
         cost_t = [c.u16 if c.u16 is not None else c.f64 for c in sc.shards]
         evolve_sharded([s.data_ptr() for s in sharded.shards], [t.data_ptr() for t in cost_t], sc.shards[0], n, k,
                        mixer, params, init, rank=-1)
-        sharded.exchange_count += 2 * params.p  # the reference's logical count (Alg. 4)
-        instrumentation.bump("exchange", 2 * params.p)
+        ex = _logical_exchanges(mixer, n, k, params.p)  # the reference's logical count
+        sharded.exchange_count += ex
+        instrumentation.bump("exchange", ex)
         return DistributedResult(sharded, sc, dc)
     for gamma, beta in zip(params.gammas, params.betas):
         if mixer.kind == "custom" and k > 0 and fused and k <= 4:
@@ -642,8 +653,9 @@ class ShardedQaoaSimulator:
                        flags=self._flag_ptrs, epoch=self._epoch, err_ptr=self._flags.data_ptr() + 4 * K,
                        expectation_out=exp)
         # the reference's logical exchange count (Alg. 4: two per X layer)
-        self.exchange_count += 2 * params.p
-        instrumentation.bump("exchange", 2 * params.p)
+        ex = _logical_exchanges(self.mixer, n, self.k, params.p)
+        self.exchange_count += ex
+        instrumentation.bump("exchange", ex)
         self._state = psi
         if not expectation:
             return None
@@ -688,6 +700,8 @@ class ShardedQaoaSimulator:
 
     def _simulate_xy(self, params: QaoaParams, initial_weight: int, expectation: bool):
         nl = self.n_local
+        if self.global_mode == "fused" and self.k > 0 and nl >= 12:
+            return self._simulate_fused(params, initial_weight, expectation)
         edges = ring_edges(self.n) if self.mixer.kind == "xy-ring" else complete_edges(self.n)
         psi = self.initial_state(initial_weight)
         for g, b in zip(params.gammas, params.betas):

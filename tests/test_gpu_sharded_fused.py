@@ -72,3 +72,34 @@ def test_sharded_custom_mixer_vs_oracle(n, K):
 def test_sharded_zero_layers():
     res = D.simulate_qaoa_distributed(labs_terms(14), QaoaParams((), ()), 4)
     np.testing.assert_allclose(res.statevector(), np.full(1 << 14, 2 ** -7), rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("kind,n,K,p", [("xy-ring", 14, 2, 2), ("xy-ring", 17, 8, 3), ("xy-complete", 14, 4, 1),
+                                        ("xy-complete", 16, 8, 2), ("xy-complete", 15, 2, 2)])
+def test_sharded_xy_matches_single_gpu(kind, n, K, p):
+    """XY mixers: the tiled XY plan over all n qubits; passes holding global
+    qubits span the shards they cover (replaces park-and-exchange per global pair)."""
+    from paper_2309_04841_b200 import hamming_weight_state
+    from paper_2309_04841_b200.problems import portfolio_terms
+
+    rng = np.random.default_rng(3 * n + K)
+    params = _params(rng, p)
+    poly = portfolio_terms(n)
+    init = hamming_weight_state(n, n // 2)
+    single = simulate_qaoa(poly, params, mixer=kind, initial=init)
+    res = D.simulate_qaoa_distributed(poly, params, K, mixer=kind, initial=init)
+    np.testing.assert_allclose(res.statevector(), single.state, rtol=0, atol=1e-12)
+    assert res.expectation() == pytest.approx(float(single._expectation_dev.item()), rel=1e-10, abs=1e-12)
+
+
+def test_sharded_xy_exchange_count_matches_reference_path():
+    from paper_2309_04841_b200 import hamming_weight_state
+    from paper_2309_04841_b200.problems import portfolio_terms
+
+    n, K = 14, 4
+    params = QaoaParams((0.2,), (0.4,))
+    init = hamming_weight_state(n, 7)
+    a = D.simulate_qaoa_distributed(portfolio_terms(n), params, K, mixer="xy-ring", initial=init)
+    r = D.simulate_qaoa_distributed(portfolio_terms(n), params, K, mixer="xy-ring", initial=init, fused=False)
+    assert a.exchange_count == r.exchange_count
+    np.testing.assert_allclose(a.statevector(), r.statevector(), rtol=0, atol=1e-12)

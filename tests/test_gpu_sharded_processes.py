@@ -64,7 +64,8 @@ def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange", dev_barrie
                           (19, 2, "x", None, "p2p", False), (15, 2, "custom", None, "p2p", True),
                           (15, 2, "custom", None, "exchange", True),
                           (16, 3, "x", None, "fused", True), (21, 5, "x", None, "fused", True),
-                          (15, 2, "custom", None, "fused", True), (14, 3, "xf", None, "fused", True)])
+                          (15, 2, "custom", None, "fused", True), (14, 3, "xf", None, "fused", True),
+                          (14, 2, "xy-ring", None, "fused", True), (15, 1, "xy-complete", None, "fused", True)])
 def test_two_process_sharded_matches_single_gpu(n, p, kind, chunk, mode, dev_barrier):
     from oracle import oracle as O
     from paper_2309_04841_b200 import Mixer, QaoaSimulator, hamming_weight_state
