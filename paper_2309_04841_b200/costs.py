@@ -54,7 +54,10 @@ class DeviceCosts:
         if isinstance(costs, torch.Tensor):
             t = costs.to(device=dev, dtype=torch.float64).contiguous()
         else:
-            t = torch.from_numpy(np.ascontiguousarray(costs, dtype=np.float64)).to(dev)
+            arr = np.ascontiguousarray(costs, dtype=np.float64)
+            if not arr.flags.writeable:  # e.g. the reference's read-only memoised diagonal (qaoa.py:74)
+                arr = arr.copy()
+            t = torch.from_numpy(arr).to(dev)
         n = t.numel().bit_length() - 1
         dc = cls(n, f64=t)
         if compact:
