@@ -67,11 +67,20 @@ def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange", dev_barrie
                           (15, 2, "custom", None, "fused", True), (14, 3, "xf", None, "fused", True),
                           (14, 2, "xy-ring", None, "fused", True), (15, 1, "xy-complete", None, "fused", True)])
 def test_two_process_sharded_matches_single_gpu(n, p, kind, chunk, mode, dev_barrier):
+    _run_processes(2, n, p, kind, chunk, mode, dev_barrier)
+
+
+@pytest.mark.parametrize("n,p,kind", [(15, 3, "x"), (15, 2, "xy-complete"), (16, 2, "custom")])
+def test_four_process_fused_matches_single_gpu(n, p, kind):
+    """k = 2: four ranks, four IPC-mapped shards, shard sets of the XY passes."""
+    _run_processes(4, n, p, kind, None, "fused", True)
+
+
+def _run_processes(world, n, p, kind, chunk, mode, dev_barrier):
     from oracle import oracle as O
     from paper_2309_04841_b200 import Mixer, QaoaSimulator, hamming_weight_state
     from paper_2309_04841_b200.problems import labs_terms, portfolio_terms
 
-    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
