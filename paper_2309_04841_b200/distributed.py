@@ -291,6 +291,28 @@ def global_su2_pass(shard_ptrs: Sequence[int], k: int, shard_size: int, part: in
     _lib.call("fq_global_su2_pass", ptrs, k, shard_size, part, parts, coef.ctypes.data, _lib.stream())
 
 
+def cost_consensus(allv, mine):
+    """One cost encoding for all shards of a fused sharded program.
+
+    ``allv[r]`` = (has_u16, has_f64, scale, offset, top) of rank r's shard
+    (top = decoded value of its highest level); ``mine`` = this rank's.
+    Returns (kind, offset, levels, delta): uint16 when every shard has
+    levels on one scale and the union range fits 16 bits — the common origin
+    is the global minimum and this rank's levels move up by ``delta`` — else
+    float64 (then every shard must have kept it)."""
+    if all(v[0] for v in allv) and len({v[2] for v in allv}) == 1:
+        scale = allv[0][2]
+        lo = min(v[3] for v in allv)
+        hi = max(v[4] for v in allv)
+        levels = int(round((hi - lo) / scale)) + 1
+        if levels <= 65536:
+            return _lib.COST_U16, lo, levels, int(round((mine[3] - lo) / scale))
+    if not all(v[1] for v in allv):
+        raise MemoryError("sharded cost encodings disagree and the float64 diagonal was not kept "
+                          "(use global_mode='p2p' or 'exchange')")
+    return _lib.COST_F64, 0.0, 0, 0
+
+
 def _logical_exchanges(mixer: Mixer, n: int, k: int, p: int) -> int:
     """The reference's exchange count for p layers (API contract): Alg. 4's two
     per X / custom layer, two per gate touching a global qubit for XY mixers
@@ -612,23 +634,13 @@ class ShardedQaoaSimulator:
                 dc.offset + (dc.levels - 1) * dc.scale if dc.u16 is not None else 0.0)
         allv = [None] * self.K
         dist.all_gather_object(allv, mine, group=self.group)
-        if all(v[0] for v in allv) and len({v[2] for v in allv}) == 1:
-            scale = allv[0][2]
-            lo = min(v[3] for v in allv)
-            hi = max(v[4] for v in allv)
-            levels = int(round((hi - lo) / scale)) + 1
-            if levels <= 65536:
-                delta = int(round((dc.offset - lo) / scale))
-                if delta:
-                    _lib.call("fq_rebase_u16", dc.u16.data_ptr(), dc.u16.numel(), -delta, _lib.stream())
-                dc.offset = lo
-                dc.levels = levels
-                self._cost_kind = _lib.COST_U16
-                return
-        if not all(v[1] for v in allv):
-            raise MemoryError("sharded cost encodings disagree and the float64 diagonal was not kept "
-                              "(use global_mode='p2p' or 'exchange')")
-        self._cost_kind = _lib.COST_F64
+        kind, offset, levels, delta = cost_consensus(allv, mine)
+        self._cost_kind = kind
+        if kind == _lib.COST_U16:
+            if delta:
+                _lib.call("fq_rebase_u16", dc.u16.data_ptr(), dc.u16.numel(), -delta, _lib.stream())
+            dc.offset = offset
+            dc.levels = levels
 
     def _cost_tensor(self) -> torch.Tensor:
         return self.costs.u16 if self._cost_kind == _lib.COST_U16 else self.costs.f64

@@ -208,3 +208,23 @@ def test_xy_planner_and_host_program_without_gpu():
             d.psi, d.n, d.cost_kind, d.costs, d.mixer = 0x1000, n, 0, 0x2000, mixer
             d.n_layers, d.layers, d.scratch = 2, lay, 0x3000
             assert lib.fq_qaoa_evolve(ctypes.byref(d), None) == _lib.FQ_ERR_CUDA
+
+
+def test_sharded_cost_consensus():
+    from paper_2309_04841_b200.distributed import cost_consensus
+
+    # two uint16 shards on one scale: common origin = global minimum, levels = union range
+    a = (True, True, 0.5, -3.0, 10.0)
+    b = (True, True, 0.5, -1.0, 20.0)
+    assert cost_consensus([a, b], b) == (_lib.COST_U16, -3.0, 47, 4)
+    assert cost_consensus([a, b], a) == (_lib.COST_U16, -3.0, 47, 0)
+    # scales disagree -> float64 everywhere (kept)
+    c = (True, True, 1.0, 0.0, 5.0)
+    assert cost_consensus([a, c], a)[0] == _lib.COST_F64
+    # union range beyond 16 bits -> float64
+    d = (True, True, 1.0, 0.0, 40000.0)
+    e = (True, True, 1.0, -40000.0, 0.0)
+    assert cost_consensus([d, e], d)[0] == _lib.COST_F64
+    # a shard without uint16 levels and another without float64: no common encoding
+    with pytest.raises(MemoryError):
+        cost_consensus([(False, True, 1.0, 0.0, 0.0), (True, False, 1.0, 0.0, 3.0)], a)
