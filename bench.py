@@ -417,7 +417,8 @@ def main():
         line = {
             **({"validation_only": "all ranks on one GPU (FQ_BENCH_ONE_DEVICE)"} if one_device else {}),
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if args.n else "weak",  # --qubits fixes the total problem
             "vs_baseline": None, "dtype": args.state, "data": "synthetic",
             "config": {"workload": f"LABS n={n} p={p} X-mixer {'complex64' if c64 else 'complex128'} objective evaluation"
                                    + (f" sharded over {world} GPUs (n_local={n_local}; value in n=26-equivalent "
