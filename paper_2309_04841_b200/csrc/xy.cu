@@ -359,7 +359,30 @@ static std::vector<XyPassPlan> plan_xy_with(int n, const std::vector<std::pair<i
         return (int)q.size() <= kTileBits && run_bits_of(tile_for(n, q)) >= min_run;
     };
     std::vector<XyPassPlan> plans;
+    // consecutive groups over the same tile become one pass (the row cap can
+    // end a group early while the next one still fits the same 12 bits)
+    auto qubits_of = [&](const std::vector<int> &g) {
+        std::vector<int> q;
+        for (int gi : g)
+            for (int x : {gates[gi].first, gates[gi].second})
+                if (std::find(q.begin(), q.end(), x) == q.end()) q.push_back(x);
+        return q;
+    };
+    std::vector<std::vector<int>> groups;
     for (auto &pg : cut_groups(gates, all, pass_fits, row_cap)) {
+        if (!groups.empty()) {
+            std::vector<int> q = qubits_of(groups.back()), q2 = qubits_of(pg);
+            std::vector<int> u = q;
+            for (int x : q2)
+                if (std::find(u.begin(), u.end(), x) == u.end()) u.push_back(x);
+            if (pass_fits(u) && tile_for(n, u) == tile_for(n, q)) {
+                groups.back().insert(groups.back().end(), pg.begin(), pg.end());
+                continue;
+            }
+        }
+        groups.push_back(pg);
+    }
+    for (auto &pg : groups) {
         XyPassPlan pl;
         std::vector<int> q;
         for (int gi : pg) {
