@@ -244,6 +244,24 @@ def main():
         dc = sim.device_costs
     else:
         sim = ShardedQaoaSimulator(poly, global_mode=args.global_mode)
+        if args.global_mode == "fused":
+            # the fused mode maps every rank's shard over CUDA IPC; if that is not
+            # possible on this node, all ranks fall back to NCCL exchanges together
+            ok = 1
+            try:
+                sim.simulate_qaoa(g, b, expectation=False)
+                torch.cuda.synchronize()
+                sim.check_barrier()
+            except Exception as exc:  # noqa: BLE001 - reported, then the exchange path runs
+                print(f"[bench] rank {rank}: fused sharded mode failed ({type(exc).__name__}: {exc}); "
+                      f"falling back to global_mode='exchange'", file=sys.stderr, flush=True)
+                ok = 0
+            flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                args.global_mode = "exchange"
+                args.fallback = True
+                sim = ShardedQaoaSimulator(poly, global_mode="exchange")
         dc = sim.costs
     barrier()
     precompute_s = time.perf_counter() - t0
@@ -434,7 +452,9 @@ def main():
                                           "exchange": "NCCL all-to-all"}[args.global_mode])
                                       if world > 1 else "single GPU",
                        **({"nvlink_bytes_per_step": nvlink_bytes, "spanning_passes_per_step": gp.value}
-                          if world > 1 and args.global_mode == "fused" else {})},
+                          if world > 1 and args.global_mode == "fused" else {}),
+                       **({"fallback": "fused mode failed on this node; NCCL exchange path measured"}
+                          if getattr(args, "fallback", False) else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                          "kernel": "k_pass16 (every tiled pass of the step; per-launch CUDA events)",
