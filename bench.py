@@ -191,7 +191,7 @@ def main():
                     help="N>1: one sharded program whose global-qubit passes span all shards over peer memory "
                          "(fused), a per-layer peer-memory global kernel (p2p), or NCCL all-to-all exchanges")
     ap.add_argument("--state", default="c128", choices=["c128", "c64"],
-                    help="state type: complex128 (the headline, the reference's) or the optional complex64 (N=1)")
+                    help="state type: complex128 (the headline, the reference's) or the optional complex64")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -237,14 +237,15 @@ def main():
     t0 = time.perf_counter()
     poly = labs_terms(n)
     c64 = args.state == "c64"
-    if c64 and world > 1:
-        raise SystemExit("--state c64 is a single-GPU option")
+    if c64 and world > 1 and args.global_mode != "fused":
+        raise SystemExit("--state c64 on several GPUs needs --global-mode fused")
     if world == 1:
         sim = QaoaSimulator(terms=poly, dtype=torch.complex64 if c64 else torch.complex128)
         dc = sim.device_costs
     else:
-        sim = ShardedQaoaSimulator(poly, global_mode=args.global_mode)
-        if args.global_mode == "fused":
+        sim = ShardedQaoaSimulator(poly, global_mode=args.global_mode,
+                                   dtype=torch.complex64 if c64 else torch.complex128)
+        if args.global_mode == "fused" and not c64:
             # the fused mode maps every rank's shard over CUDA IPC; if that is not
             # possible on this node, all ranks fall back to NCCL exchanges together
             ok = 1

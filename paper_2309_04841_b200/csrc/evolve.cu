@@ -739,7 +739,8 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCt
             int k = mask_class(sq, P.maskA);
             int mbv = (mix == MIX_RX && !seq_heavy(sq) && mb != 2) ? 3 : mb;
             if (mix == MIX_SU2) mbv = mb == 2 ? 2 : 3;
-            const int s = d->cost_kind == FQ_COST_U16
+            const int s = c64 ? launch_pass_global_c64(d->cost_kind, P, M, sq, ph, ma, mbv, k, ggrid, st)
+                          : d->cost_kind == FQ_COST_U16
                               ? launch_pass_global_u16(mix, P, M, sq, ph, mix == MIX_SU2 ? 0 : ma, mbv, k, ggrid, st)
                               : launch_pass_global_f64(mix, P, M, sq, ph, mix == MIX_SU2 ? 0 : ma, mbv, k, ggrid, st);
             if (s) return s;
@@ -968,7 +969,8 @@ int fq_qaoa_evolve_sharded(const fq_evolve_desc *d, const fq_shard_desc *s, void
     FQ_CHECK_ARG(s->rank >= -1 && s->rank < K, "fq_qaoa_evolve_sharded: bad rank %d", s->rank);
     FQ_CHECK_ARG(d->n >= kTileBits && d->n + s->k <= 40, "fq_qaoa_evolve_sharded: n_local=%d must be >= %d", d->n,
                  kTileBits);
-    FQ_CHECK_ARG(d->state_kind == FQ_STATE_C128, "fq_qaoa_evolve_sharded: complex128 states only");
+    FQ_CHECK_ARG(d->state_kind == FQ_STATE_C128 || (d->state_kind == FQ_STATE_C64 && d->mixer == FQ_MIXER_X),
+                 "fq_qaoa_evolve_sharded: complex128 states, or complex64 under the X mixer");
     FQ_CHECK_ARG(d->mixer >= FQ_MIXER_X && d->mixer <= FQ_MIXER_CUSTOM, "fq_qaoa_evolve_sharded: bad mixer");
     FQ_CHECK_ARG(d->mixer != FQ_MIXER_CUSTOM || d->su2, "fq_qaoa_evolve_sharded: custom mixer needs su2 table");
     FQ_CHECK_ARG(d->n_layers >= 0 && (d->n_layers == 0 || d->layers), "fq_qaoa_evolve_sharded: bad layers");

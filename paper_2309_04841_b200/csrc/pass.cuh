@@ -617,6 +617,9 @@ int launch_pass_global_u16(int mix, const PassParams &P, const PassMaps &M, int 
                            int grid, cudaStream_t st);
 int launch_pass_global_f64(int mix, const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k,
                            int grid, cudaStream_t st);
+// sharded complex64 states (G = true, R = float): X mixer (pass_global_c64.cu)
+int launch_pass_global_c64(int cost, const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k,
+                           int grid, cudaStream_t st);
 // complex64 states (R = float): X mixer, all round programs, one unit per cost encoding
 int launch_pass_c64_u16(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
 int launch_pass_c64_f64(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);

@@ -32,7 +32,7 @@ import torch.distributed as dist
 from . import _lib, instrumentation
 from .costs import DeviceCosts
 from .mixers import SU2, Mixer, complete_edges, ring_edges, run_program, su2_table
-from .qaoa import QaoaParams, QaoaResult, _initial_state, resolve_costs
+from .qaoa import QaoaParams, QaoaResult, _initial_state, resolve_costs, state_dtype
 from .statevec import expectation_device, overlap_device
 from .terms import TermPolynomial
 
@@ -325,7 +325,8 @@ def _logical_exchanges(mixer: Mixer, n: int, k: int, p: int) -> int:
 
 def evolve_sharded(shard_ptrs: Sequence[int], cost_ptrs: Sequence[int], costs: DeviceCosts, n: int, k: int,
                    mixer: Mixer, params: QaoaParams, init: bool, rank: int = -1, flags=None, epoch=None,
-                   err_ptr: int | None = None, expectation_out: torch.Tensor | None = None) -> None:
+                   err_ptr: int | None = None, expectation_out: torch.Tensor | None = None,
+                   dtype: torch.dtype = torch.complex128) -> None:
     """libfqaoa fq_qaoa_evolve_sharded: the whole p-layer program on a state
     sharded by its top k qubits — local groups as passes on each shard, the
     global group as peer-memory passes over all shards, fused across layers.
@@ -354,6 +355,7 @@ def evolve_sharded(shard_ptrs: Sequence[int], cost_ptrs: Sequence[int], costs: D
     desc.init_amp = 1.0 / sqrt(float(2 ** n)) if init else 0.0
     desc.expectation_dev = expectation_out.data_ptr() if expectation_out is not None else None
     desc.scratch = _lib.scratch().data_ptr()
+    desc.state_kind = _lib.STATE_C64 if dtype == torch.complex64 else _lib.STATE_C128
     sd = _lib.FqShardDesc()
     sd.k = k
     sd.rank = rank
@@ -371,7 +373,7 @@ def evolve_sharded(shard_ptrs: Sequence[int], cost_ptrs: Sequence[int], costs: D
 
 
 def simulate_qaoa_distributed(problem, params: QaoaParams, K: int, mixer: "str | Mixer" = "x",
-                              initial=None, fused: bool = True) -> DistributedResult:
+                              initial=None, fused: bool = True, dtype=None) -> DistributedResult:
     """K logical workers on the current GPU (reference distributed.py:280-296).
     For the X mixer, phase + local qubits run as one fused program per shard;
     the global qubits run in one peer-memory pass over all shards (``fused``;
@@ -379,9 +381,16 @@ def simulate_qaoa_distributed(problem, params: QaoaParams, K: int, mixer: "str |
     dc, n = resolve_costs(problem)
     mixer = Mixer.parse(mixer)
     k = _validate_split(n, K)
-    state, init = _initial_state(n, mixer, initial)
+    dtype = state_dtype(dtype)
+    if dtype == torch.complex64 and not (fused and 1 <= k <= 3 and n - k >= 12 and mixer.kind == "x"):
+        raise ValueError("complex64 sharded states run the fused program: X mixer, K = 2..8, >= 12 qubits per shard")
+    state, init = _initial_state(n, mixer, initial, dtype=dtype)
+    if init and dtype == torch.complex64:
+        init_fn = "fq_init_state_c64"
+    else:
+        init_fn = "fq_init_state"
     if init:
-        _lib.call("fq_init_state", state.data_ptr(), state.numel(), -1, 1.0 / sqrt(float(1 << n)), 0, _lib.stream())
+        _lib.call(init_fn, state.data_ptr(), state.numel(), -1, 1.0 / sqrt(float(1 << n)), 0, _lib.stream())
     sharded = ShardedState(n, k, list(state.view(K, -1).unbind(0)))
     sc = ShardedCosts(n, k, _slice_device_costs(dc, K))
     n_local = n - k
@@ -390,7 +399,7 @@ def simulate_qaoa_distributed(problem, params: QaoaParams, K: int, mixer: "str |
         # (the same kernels a multi-GPU rank runs over peer memory)
         cost_t = [c.u16 if c.u16 is not None else c.f64 for c in sc.shards]
         evolve_sharded([s.data_ptr() for s in sharded.shards], [t.data_ptr() for t in cost_t], sc.shards[0], n, k,
-                       mixer, params, init, rank=-1)
+                       mixer, params, init, rank=-1, dtype=dtype)
         ex = _logical_exchanges(mixer, n, k, params.p)  # the reference's logical count
         sharded.exchange_count += ex
         instrumentation.bump("exchange", ex)
@@ -440,18 +449,23 @@ class ShardedQaoaSimulator:
 
     def __init__(self, poly: TermPolynomial, group=None, mixer: "str | Mixer" = "x",
                  compact: bool = True, keep_f64: bool | None = None, chunk_bytes: int | None = None,
-                 local_ops=None, global_mode: str = "exchange", device_barrier: bool = True):
+                 local_ops=None, global_mode: str = "exchange", device_barrier: bool = True, dtype=None):
+        """``dtype``: complex128 (default) or complex64 (global_mode="fused",
+        X mixer: half the memory per rank, e.g. n = 35 on two B200s)."""
         self.group = group
+        self.dtype = state_dtype(dtype)
         self.K = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.n = poly.n
         self.k = _validate_split(self.n, self.K)
         self.n_local = self.n - self.k
         self.mixer = Mixer.parse(mixer)
+        if self.dtype == torch.complex64 and (global_mode != "fused" or self.mixer.kind != "x" or self.k == 0):
+            raise ValueError("complex64 sharded states need global_mode='fused', the X mixer and >= 2 ranks")
         self.ops = local_ops if local_ops is not None else CudaLocalOps()
         base = self.rank << self.n_local
         if keep_f64 is None:
-            keep_f64 = self.ops.fits(self.n_local, 8 + 16 * 2 + 2)
+            keep_f64 = self.ops.fits(self.n_local, 8 + (8 + 2 if self.dtype == torch.complex64 else 16 * 2 + 2))
         self.costs = self.ops.precompute(poly, base, self.n_local, compact, keep_f64)
         instrumentation.bump("precompute")
         self.exchange_count = 0
@@ -569,7 +583,8 @@ class ShardedQaoaSimulator:
         all-gathered once).  NVLink peers on one node; on one device (tests)
         the same IPC path maps another process's allocation."""
         if self._p2p_buf is None:
-            self._p2p_buf = self.ops.empty(self.n_local)
+            self._p2p_buf = (torch.empty(1 << self.n_local, dtype=torch.complex64, device=_lib.device())
+                             if self.dtype == torch.complex64 else self.ops.empty(self.n_local))
             # flag arrays of the device-side barrier (K uint32 slots per rank) + error word
             self._flags = torch.zeros(self.K + 1, dtype=torch.int32, device=self._p2p_buf.device)
             torch.cuda.synchronize()  # zeroed before any peer can store into it
@@ -663,7 +678,7 @@ class ShardedQaoaSimulator:
             DeviceCosts(nl, f64=self.costs.f64)
         evolve_sharded(self._peers, self._cost_peers, view, n, self.k, self.mixer, params, init, rank=self.rank,
                        flags=self._flag_ptrs, epoch=self._epoch, err_ptr=self._flags.data_ptr() + 4 * K,
-                       expectation_out=exp)
+                       expectation_out=exp, dtype=self.dtype)
         # the reference's logical exchange count (Alg. 4: two per X layer)
         ex = _logical_exchanges(self.mixer, n, self.k, params.p)
         self.exchange_count += ex

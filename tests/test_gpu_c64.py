@@ -139,3 +139,25 @@ def test_c64_headline_config_vs_reference_fingerprint(golden_large):
     blocks = (np.abs(state.astype(np.complex128)) ** 2).reshape(1024, -1).sum(axis=1)
     ref_blocks = golden_large[f"{name}/block_norm2"]
     np.testing.assert_allclose(blocks, ref_blocks, rtol=TOL, atol=0)
+
+
+@pytest.mark.parametrize("n,K,p", [(14, 2, 3), (16, 8, 2), (20, 4, 4)])
+def test_c64_sharded_in_process_vs_single(n, K, p):
+    """complex64 under the fused sharded program (spanning passes with R = float)."""
+    from paper_2309_04841_b200.distributed import simulate_qaoa_distributed
+
+    rng = np.random.default_rng(n + K)
+    params = QaoaParams(tuple(rng.uniform(-1, 1, p)), tuple(rng.uniform(-1.6, 1.6, p)))
+    poly = labs_terms(n)
+    res = simulate_qaoa_distributed(poly, params, K, dtype="complex64")
+    single = simulate_qaoa(poly, params, dtype="complex64")
+    costs = single.costs
+    ref = O.simulate(costs, params.gammas, params.betas)
+    got = res.statevector()
+    assert got.dtype == np.complex64
+    _check_state(got, ref)
+    np.testing.assert_allclose(got, single.state, rtol=0, atol=1e-6 * np.abs(ref).max())
+    _check_energy(res.expectation(), O.expectation(ref, costs), costs)
+    with pytest.raises(ValueError):
+        simulate_qaoa_distributed(poly, params, K, mixer="xy-ring", dtype="complex64",
+                                  initial=np.full(1 << n, 2 ** (-n / 2)))

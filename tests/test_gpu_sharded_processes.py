@@ -32,7 +32,7 @@ def _mixer(kind, n):
                                       for j in range(n)])
 
 
-def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange", dev_barrier=True):
+def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange", dev_barrier=True, dtype=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -47,7 +47,7 @@ def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange", dev_barrie
         if kind == "xf":  # float64 costs under the X mixer
             kind = "x"
         sim = ShardedQaoaSimulator(poly, mixer=_mixer(kind, n), chunk_bytes=chunk, global_mode=mode,
-                                   device_barrier=dev_barrier)
+                                   device_barrier=dev_barrier, dtype=dtype)
         E = sim.simulate_qaoa(g, b, initial_weight=n // 2 if kind.startswith("xy") else None)
         ov = sim.overlap()
         q.put((rank, E, ov, sim.exchange_count, sim.shard.cpu().numpy()))
@@ -76,7 +76,11 @@ def test_four_process_fused_matches_single_gpu(n, p, kind):
     _run_processes(4, n, p, kind, None, "fused", True)
 
 
-def _run_processes(world, n, p, kind, chunk, mode, dev_barrier):
+def test_two_process_fused_complex64():
+    _run_processes(2, 16, 3, "x", None, "fused", True, dtype="complex64")
+
+
+def _run_processes(world, n, p, kind, chunk, mode, dev_barrier, dtype=None):
     from oracle import oracle as O
     from paper_2309_04841_b200 import Mixer, QaoaSimulator, hamming_weight_state
     from paper_2309_04841_b200.problems import labs_terms, portfolio_terms
@@ -84,7 +88,7 @@ def _run_processes(world, n, p, kind, chunk, mode, dev_barrier):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, p, kind, chunk, q, mode, dev_barrier))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, p, kind, chunk, q, mode, dev_barrier, dtype))
              for r in range(world)]
     for pr in procs:
         pr.start()
@@ -100,9 +104,10 @@ def _run_processes(world, n, p, kind, chunk, mode, dev_barrier):
     init = hamming_weight_state(n, n // 2) if kind.startswith("xy") else None
     res = sim.simulate_qaoa(g, b, initial=init)
     full = np.concatenate([o[4] for o in out])
-    np.testing.assert_allclose(full, res.state, rtol=0, atol=1e-12)
+    tol = 1e-12 if dtype is None else 1e-4 * np.abs(res.state).max()  # complex64: the fp32 tolerance
+    np.testing.assert_allclose(full, res.state, rtol=0, atol=tol)
     for rank, E, ov, ex, _ in out:
-        assert E == pytest.approx(sim.get_expectation(res), rel=1e-10, abs=1e-12)
-        assert ov == pytest.approx(sim.get_overlap(res), abs=1e-12)
+        assert E == pytest.approx(sim.get_expectation(res), rel=1e-10 if dtype is None else 1e-4, abs=1e-12)
+        assert ov == pytest.approx(sim.get_overlap(res), abs=1e-12 if dtype is None else 1e-4)
         if kind in ("x", "custom"):
             assert ex == 2 * p  # Alg. 4: two exchanges per layer
