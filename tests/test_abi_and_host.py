@@ -63,6 +63,10 @@ def test_no_cpu_fallback():
 
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         QaoaSimulator(terms=labs_terms(4))
+    from paper_2309_04841_b200 import _kernels
+
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _kernels.warm_up()
 
 
 def _plan(n, p, state_kind=0):
