@@ -381,7 +381,7 @@ static int run_bits_of(const Group &g) {
 static double run_factor(long long run_bytes, bool heavy) {
     if (run_bytes >= 512) return 1.0;
     if (run_bytes >= 256) return heavy ? 1.13 : 1.04;
-    if (run_bytes >= 128) return heavy ? 2.0 : 1.18;
+    if (run_bytes >= 128) return heavy ? 1.25 : 1.15;
     if (run_bytes >= 64) return heavy ? 3.9 : 2.33;
     return heavy ? 8.0 : 4.7;
 }
