@@ -811,6 +811,7 @@ static int g_xy_tiled = 1;   // tiled XY passes (0: one pair kernel per gate, th
 extern int g_xy_min_run;     // xy.cu
 extern int g_xy_row_cap;     // xy.cu
 extern int g_xy_pad;         // xy.cu
+extern int g_xy_prefetch;    // xy.cu
 
 static int run_xy_program(const fq_evolve_desc *d, cudaStream_t st) {
     const int n = d->n;
@@ -1024,6 +1025,7 @@ int fq_set_option(const char *name, int value) {
         {"xy_min_run", &g_xy_min_run, 0, 8},  // XY pass tiles: min contiguous run, log2 amplitudes (0 = auto)
         {"xy_row_cap", &g_xy_row_cap, 0, 64},  // XY pass cut: new qubits per leading qubit (0 = auto)
         {"xy_pad", &g_xy_pad, 0, 1},        // XY passes: gate-free load / store rounds for coalescing
+        {"xy_prefetch", &g_xy_prefetch, -1, 1},  // XY passes: L2 tensor prefetch (-1: runs >= 256 B)
         {"probe", &g_probe, 0, 7},          // development: isolate phase costs (results invalid when != 0)
     };
     for (auto &o : opts) {

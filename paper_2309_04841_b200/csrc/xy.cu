@@ -22,6 +22,7 @@
 namespace fq {
 
 constexpr int kXyMaxRounds = 24;
+int g_xy_prefetch = 1;  // option xy_prefetch: L2 tensor prefetch of XY tiles (-1: runs >= 256 B only; measured: always on is best)
 int g_xy_pad = 1;      // option xy_pad: gate-free first / last rounds keep loads and stores on tile bits 0..4
 int g_xy_min_run = 0;  // minimum contiguous run (log2 amplitudes) of an XY pass tile; 0 = chosen by the cost model
 constexpr int kXyMaxGates = 6;  // C(4, 2): distinct pairs of one 4-bit register set
@@ -682,7 +683,9 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
                     P->partials = d->scratch + launches;
                     XyMaps M;
                     std::memset(&M, 0, sizeof M);
-                    P->pf = 1;
+                    // tensor prefetch of the next tile (XY passes, unlike the X passes, gain from it at
+                    // 128-B runs too: 2.22 vs 2.32 ms per ring layer at n = 26)
+                    P->pf = g_xy_prefetch >= 0 ? g_xy_prefetch : ((16 << run_bits_of(pl.tile)) >= 256 ? 1 : 0);
                     P->sm_rank = cached_tile_map(&M.state, P->psi, nl, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2,
                                                 P->sm_shift, P->sm_bits);
                     P->cm_rank = 0;
