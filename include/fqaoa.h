@@ -195,7 +195,7 @@ typedef struct fq_evolve_desc {
     double *expectation_dev;  /* if non-NULL: sum_k c_k |psi_k|^2 of the final state  */
     double *scratch;      /* device, >= FQ_SCRATCH_DOUBLES doubles                   */
     int state_kind;       /* FQ_STATE_C128 (default, zero) / FQ_STATE_C64: psi is
-                             complex64[2^n]; X mixer, n > 12 (tiled passes)          */
+                             complex64[2^n]; X / custom mixers, n > 12               */
 } fq_evolve_desc;
 
 /* Runs the whole p-layer program: phase fused into the first mixer pass of

@@ -518,7 +518,9 @@ static int mask_class(int seq, const unsigned char *maskA) {
 static int launch_pass(int mix, int cost, bool c64, const PassParams &P, const PassMaps &M, int seq, int ph, int ma,
                        int mb, int grid, cudaStream_t st) {
     const int k = mask_class(seq, P.maskA);
-    if (mix == MIX_SU2) return launch_pass_su2(P, M, cost, seq, ph, mb == 2 ? 2 : 3, k, grid, st);
+    if (mix == MIX_SU2)
+        return c64 ? launch_pass_su2_c64(P, M, cost, seq, ph, mb == 2 ? 2 : 3, k, grid, st)
+                   : launch_pass_su2(P, M, cost, seq, ph, mb == 2 ? 2 : 3, k, grid, st);
     if (!seq_heavy(seq) && mb != 2) mb = 3;
     if (c64)
         return cost == FQ_COST_U16 ? launch_pass_c64_u16(P, M, seq, ph, ma, mb, k, grid, st)
@@ -949,9 +951,10 @@ int fq_qaoa_evolve(const fq_evolve_desc *d, void *stream) {
     FQ_CHECK_ARG(d->mixer != FQ_MIXER_CUSTOM || d->su2, "fq_qaoa_evolve: custom mixer needs su2 table");
     FQ_CHECK_ARG(!d->expectation_dev || d->scratch, "fq_qaoa_evolve: expectation needs scratch");
     FQ_CHECK_ARG(d->state_kind == FQ_STATE_C128 || d->state_kind == FQ_STATE_C64, "fq_qaoa_evolve: bad state kind");
-    if (d->state_kind == FQ_STATE_C64 && (d->n <= kTileBits || d->mixer != FQ_MIXER_X)) {
-        set_error("fq_qaoa_evolve: complex64 states run the X mixer on n > %d qubits (got n=%d, mixer=%d)", kTileBits,
-                  d->n, d->mixer);
+    if (d->state_kind == FQ_STATE_C64 &&
+        (d->n <= kTileBits || (d->mixer != FQ_MIXER_X && d->mixer != FQ_MIXER_CUSTOM))) {
+        set_error("fq_qaoa_evolve: complex64 states run the X / custom mixers on n > %d qubits (got n=%d, mixer=%d)",
+                  kTileBits, d->n, d->mixer);
         return FQ_ERR_UNSUPPORTED;
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);

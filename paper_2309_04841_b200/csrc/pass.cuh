@@ -611,6 +611,8 @@ int launch_pass_rx_u16_heavy(const PassParams &P, const PassMaps &M, int seq, in
 int launch_pass_rx_f64_light(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
 int launch_pass_rx_f64_heavy(const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k, int grid, cudaStream_t st);
 int launch_pass_su2(const PassParams &P, const PassMaps &M, int cost, int seq, int ph, int mb, int k, int grid, cudaStream_t st);
+int launch_pass_su2_c64(const PassParams &P, const PassMaps &M, int cost, int seq, int ph, int mb, int k, int grid,
+                        cudaStream_t st);
 // sharded states (G = true, complex128): passes whose tile spans the global
 // qubits; every mixer and round program, one unit per cost encoding (pass_global_*.cu)
 int launch_pass_global_u16(int mix, const PassParams &P, const PassMaps &M, int seq, int ph, int ma, int mb, int k,

@@ -161,3 +161,26 @@ def test_c64_sharded_in_process_vs_single(n, K, p):
     with pytest.raises(ValueError):
         simulate_qaoa_distributed(poly, params, K, mixer="xy-ring", dtype="complex64",
                                   initial=np.full(1 << n, 2 ** (-n / 2)))
+
+
+@pytest.mark.parametrize("n", [13, 17])
+def test_c64_custom_mixer_vs_oracle(n):
+    """Custom per-qubit SU(2) mixers on complex64 states (k_pass16<MIX_SU2, ..., float>)."""
+    from _helpers import random_su2_coeffs
+    from paper_2309_04841_b200 import SU2, Mixer
+
+    rng = np.random.default_rng(70 + n)
+    tabs = {}
+
+    def factory(beta):
+        if beta not in tabs:
+            tabs[beta] = [SU2(*random_su2_coeffs(rng)) for _ in range(n)]
+        return tabs[beta]
+
+    g, b = (0.3, -0.2, 0.4), (0.2, 0.9, -0.5)
+    sim = QaoaSimulator(terms=labs_terms(n), mixer=Mixer.custom(factory), dtype="complex64")
+    res = sim.simulate_qaoa(g, b)
+    costs = sim.get_cost_diagonal()
+    ref = O.simulate(costs, g, b, "custom", None, su2_factory=lambda beta: [(u.a, u.b) for u in factory(beta)])
+    _check_state(sim.get_statevector(res), ref)
+    _check_energy(sim.get_expectation(res), O.expectation(ref, costs), costs)
