@@ -951,9 +951,9 @@ int fq_qaoa_evolve(const fq_evolve_desc *d, void *stream) {
     FQ_CHECK_ARG(d->mixer != FQ_MIXER_CUSTOM || d->su2, "fq_qaoa_evolve: custom mixer needs su2 table");
     FQ_CHECK_ARG(!d->expectation_dev || d->scratch, "fq_qaoa_evolve: expectation needs scratch");
     FQ_CHECK_ARG(d->state_kind == FQ_STATE_C128 || d->state_kind == FQ_STATE_C64, "fq_qaoa_evolve: bad state kind");
-    if (d->state_kind == FQ_STATE_C64 &&
-        (d->n <= kTileBits || (d->mixer != FQ_MIXER_X && d->mixer != FQ_MIXER_CUSTOM))) {
-        set_error("fq_qaoa_evolve: complex64 states run the X / custom mixers on n > %d qubits (got n=%d, mixer=%d)",
+    const bool is_xy = d->mixer == FQ_MIXER_XY_RING || d->mixer == FQ_MIXER_XY_COMPLETE;
+    if (d->state_kind == FQ_STATE_C64 && (d->n <= kTileBits || (is_xy && !g_xy_tiled))) {
+        set_error("fq_qaoa_evolve: complex64 states run the tiled passes, n > %d qubits (got n=%d, mixer=%d)",
                   kTileBits, d->n, d->mixer);
         return FQ_ERR_UNSUPPORTED;
     }
@@ -973,8 +973,8 @@ int fq_qaoa_evolve_sharded(const fq_evolve_desc *d, const fq_shard_desc *s, void
     FQ_CHECK_ARG(s->rank >= -1 && s->rank < K, "fq_qaoa_evolve_sharded: bad rank %d", s->rank);
     FQ_CHECK_ARG(d->n >= kTileBits && d->n + s->k <= 40, "fq_qaoa_evolve_sharded: n_local=%d must be >= %d", d->n,
                  kTileBits);
-    FQ_CHECK_ARG(d->state_kind == FQ_STATE_C128 || (d->state_kind == FQ_STATE_C64 && d->mixer == FQ_MIXER_X),
-                 "fq_qaoa_evolve_sharded: complex128 states, or complex64 under the X mixer");
+    FQ_CHECK_ARG(d->state_kind == FQ_STATE_C128 || (d->state_kind == FQ_STATE_C64 && d->mixer != FQ_MIXER_CUSTOM),
+                 "fq_qaoa_evolve_sharded: complex128 states, or complex64 under the X / XY mixers");
     FQ_CHECK_ARG(d->mixer >= FQ_MIXER_X && d->mixer <= FQ_MIXER_CUSTOM, "fq_qaoa_evolve_sharded: bad mixer");
     FQ_CHECK_ARG(d->mixer != FQ_MIXER_CUSTOM || d->su2, "fq_qaoa_evolve_sharded: custom mixer needs su2 table");
     FQ_CHECK_ARG(d->n_layers >= 0 && (d->n_layers == 0 || d->layers), "fq_qaoa_evolve_sharded: bad layers");

@@ -36,7 +36,7 @@ struct XyRound {
 };
 
 struct XyParams {
-    double2 *psi;
+    void *psi;                // C2<R>[2^n] (complex128 or complex64)
     const void *costs;
     double cost_scale, cost_offset;
     double *partials;
@@ -56,14 +56,14 @@ struct XyParams {
     // shard k >> nl at local offset k & (2^nl - 1) (peer-mapped shard pointers)
     long long tile0;  // first tile of this launch
     int nl;
-    double2 *shard[8];
+    void *shard[8];
     const void *cshard[8];
 };
 
-template <bool G>
-__device__ __forceinline__ double2 *xy_amp(const XyParams &P, long long k) {
-    if constexpr (G) return P.shard[k >> P.nl] + (k & ((1LL << P.nl) - 1));
-    else return P.psi + k;
+template <bool G, typename T>
+__device__ __forceinline__ T *xy_amp(const XyParams &P, long long k) {
+    if constexpr (G) return static_cast<T *>(P.shard[k >> P.nl]) + (k & ((1LL << P.nl) - 1));
+    else return static_cast<T *>(P.psi) + k;
 }
 
 template <bool G, typename C>
@@ -79,20 +79,21 @@ __device__ __forceinline__ const C *xy_cost(const XyParams &P, long long k) {
 __host__ __device__ __forceinline__ int xy_slot(int e) { return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7); }
 
 // x_lo' = c x_lo - i s x_hi ; x_hi' = -i s x_lo + c x_hi   (reference _kernels.py:44-47)
-template <int A, int B>
-__device__ __forceinline__ void xy_gate(double2 (&v)[kRegs], double c, double s) {
+template <int A, int B, typename T, typename R>
+__device__ __forceinline__ void xy_gate(T (&v)[kRegs], R c, R s) {
 #pragma unroll
     for (int i = 0; i < kRegs; ++i) {
         if (((i >> A) & 1) && !((i >> B) & 1)) {
             const int j = i ^ (1 << A) ^ (1 << B);
-            const double2 xl = v[i], xh = v[j];
-            v[i] = make_double2(fma(c, xl.x, s * xh.y), fma(c, xl.y, -s * xh.x));
-            v[j] = make_double2(fma(s, xl.y, c * xh.x), fma(c, xh.y, -s * xl.x));
+            const T xl = v[i], xh = v[j];
+            v[i] = Cx<R>::make(fma(c, xl.x, s * xh.y), fma(c, xl.y, -s * xh.x));
+            v[j] = Cx<R>::make(fma(s, xl.y, c * xh.x), fma(c, xh.y, -s * xl.x));
         }
     }
 }
 
-__device__ __forceinline__ void xy_apply(double2 (&v)[kRegs], int code, double c, double s) {
+template <typename T, typename R>
+__device__ __forceinline__ void xy_apply(T (&v)[kRegs], int code, R c, R s) {
     switch (code) {
         case 1: xy_gate<0, 1>(v, c, s); break;
         case 2: xy_gate<0, 2>(v, c, s); break;
@@ -136,30 +137,36 @@ __device__ __forceinline__ long long xy_tile_base(const int *tile_pos, long long
     return base;
 }
 
-template <int COST>
-__device__ __forceinline__ double2 xy_phase(const XyParams &P, CostRaw<COST> raw, const double2 *tlo,
-                                            const double2 *thi) {
+template <int COST, typename R>
+__device__ __forceinline__ C2<R> xy_phase(const XyParams &P, CostRaw<COST> raw, const C2<R> *tlo,
+                                          const C2<R> *thi) {
     if constexpr (COST == FQ_COST_F64) {
-        return phase_f64(raw, P.gamma);
+        const double2 f = phase_f64(raw, P.gamma);
+        return Cx<R>::make((R)f.x, (R)f.y);
     } else {
-        if (P.table_hi == 0) return phase_sincos_u16(raw, P.cost_scale, P.cost_offset, P.gamma);
-        const int cp = threadIdx.x & (kCopies - 1);
-        return cmul(thi[(raw >> 6) * kCopies + cp], tlo[(raw & 63) * kCopies + cp]);
+        if (P.table_hi == 0) {
+            const double2 f = phase_sincos_u16(raw, P.cost_scale, P.cost_offset, P.gamma);
+            return Cx<R>::make((R)f.x, (R)f.y);
+        }
+        constexpr int CP = table_copies<R>();
+        const int cp = threadIdx.x & (CP - 1);
+        return cmul(thi[(raw >> 6) * CP + cp], tlo[(raw & 63) * CP + cp]);
     }
 }
 
-template <int COST, int PH, bool G = false>
+template <int COST, int PH, bool G = false, typename RT = double>
 __global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__ XyParams P,
                                                          const __grid_constant__ CUtensorMap tm_state,
                                                          const __grid_constant__ CUtensorMap tm_cost) {
-    extern __shared__ double2 smem[];
-    double2 *tile = smem;
-    double2 *tlo = smem + kTile;
-    double2 *thi = tlo + kTableLo * kCopies;
+    using T = C2<RT>;
+    extern __shared__ __align__(16) unsigned char xy_smem_raw[];
+    T *tile = reinterpret_cast<T *>(xy_smem_raw);
+    T *tlo = tile + kTile;
+    T *thi = tlo + kTableLo * table_copies<RT>();
     __shared__ double red[kThreads / 32];
     const int tid = threadIdx.x;
     if (COST == FQ_COST_U16 && PH) {
-        if (P.table_hi > 0) build_phase_tables<double>(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
+        if (P.table_hi > 0) build_phase_tables<RT>(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
         __syncthreads();
     }
     const long long thr_first = xy_tphys(P, P.rounds[0], tid);
@@ -178,13 +185,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__
                 tensor_prefetch_l2(&tm_cost, P.cm_rank, c);
             }
         }
-        double2 v[kRegs];
+        T v[kRegs];
         if (P.init) {
 #pragma unroll
-            for (int i = 0; i < kRegs; ++i) v[i] = make_double2(P.init_amp, 0.0);
+            for (int i = 0; i < kRegs; ++i) v[i] = Cx<RT>::make((RT)P.init_amp, (RT)0);
         } else {
 #pragma unroll
-            for (int i = 0; i < kRegs; ++i) v[i] = ld_stream(xy_amp<G>(P, base + thr_first + P.roff_first[i]));
+            for (int i = 0; i < kRegs; ++i) v[i] = ld_stream(xy_amp<G, T>(P, base + thr_first + P.roff_first[i]));
         }
         if (PH) {
             CostRaw<COST> raw[kRegs];
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__
             }
 #pragma unroll
             for (int i = 0; i < kRegs; ++i)
-                v[i] = cmul(v[i], xy_phase<COST>(P, raw[i], tlo, thi));
+                v[i] = cmul(v[i], xy_phase<COST, RT>(P, raw[i], tlo, thi));
         }
         for (int r = 0; r < P.nrounds; ++r) {
             const XyRound &R = P.rounds[r];
@@ -211,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__
 #pragma unroll
                 for (int i = 0; i < kRegs; ++i) v[i] = tile[sr ^ R.sreg[i]];
             }
-            for (int g = 0; g < R.ngates; ++g) xy_apply(v, R.gate[g], P.c, P.s);
+            for (int g = 0; g < R.ngates; ++g) xy_apply(v, R.gate[g], (decltype(v[0].x))P.c, (decltype(v[0].x))P.s);
         }
 #pragma unroll
         for (int i = 0; i < kRegs; ++i) {
@@ -220,9 +227,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__
                 double cv;
                 if constexpr (COST == FQ_COST_F64) cv = *xy_cost<G, double>(P, k);
                 else cv = decode_u16(*xy_cost<G, unsigned short>(P, k), P.cost_scale, P.cost_offset);
-                eacc += cv * (v[i].x * v[i].x + v[i].y * v[i].y);
+                eacc += cv * ((double)v[i].x * v[i].x + (double)v[i].y * v[i].y);
             }
-            st_stream(xy_amp<G>(P, k), v[i]);
+            st_stream(xy_amp<G, T>(P, k), v[i]);
         }
     }
     if (P.expect) {
@@ -543,19 +550,31 @@ struct XyMaps {
     alignas(64) CUtensorMap cost;
 };
 
-template <int COST, int PH, bool G = false>
+template <int COST, int PH, bool G = false, typename R = double>
 static int launch_xy(const XyParams &P, const XyMaps &M, int grid, cudaStream_t st) {
     static bool configured = false;
-    const size_t smem = (size_t)(kTile + (kTableLo + kMaxTableHi) * kCopies) * sizeof(double2);
+    constexpr int CP = table_copies<R>();
+    const size_t smem = (size_t)(kTile + (kTableLo + kMaxTableHi) * CP) * sizeof(C2<R>);
     if (!configured) {
-        cudaFuncSetAttribute(k_xy_pass<COST, PH, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_xy_pass<COST, PH, G, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    const size_t need = (size_t)(kTile + (PH && COST == FQ_COST_U16 ? (kTableLo + P.table_hi) * kCopies : 0)) *
-                        sizeof(double2);
-    k_xy_pass<COST, PH, G><<<grid, kThreads, need, st>>>(P, M.state, M.cost);
+    const size_t need = (size_t)(kTile + (PH && COST == FQ_COST_U16 ? (kTableLo + P.table_hi) * CP : 0)) *
+                        sizeof(C2<R>);
+    k_xy_pass<COST, PH, G, R><<<grid, kThreads, need, st>>>(P, M.state, M.cost);
     FQ_LAUNCHED("k_xy_pass");
     return FQ_OK;
+}
+
+// every (cost, phase, spanning) combination for one real type
+template <typename R>
+static int launch_xy_any(int cost, bool ph, bool g, const XyParams &P, const XyMaps &M, int grid, cudaStream_t st) {
+    if (cost == FQ_COST_U16) {
+        if (g) return ph ? launch_xy<FQ_COST_U16, 1, true, R>(P, M, grid, st) : launch_xy<FQ_COST_U16, 0, true, R>(P, M, grid, st);
+        return ph ? launch_xy<FQ_COST_U16, 1, false, R>(P, M, grid, st) : launch_xy<FQ_COST_U16, 0, false, R>(P, M, grid, st);
+    }
+    if (g) return ph ? launch_xy<FQ_COST_F64, 1, true, R>(P, M, grid, st) : launch_xy<FQ_COST_F64, 0, true, R>(P, M, grid, st);
+    return ph ? launch_xy<FQ_COST_F64, 1, false, R>(P, M, grid, st) : launch_xy<FQ_COST_F64, 0, false, R>(P, M, grid, st);
 }
 
 // Whole XY program (n >= 13): p x (phase, gate sequence), expectation.
@@ -587,7 +606,12 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
     if (!sh) mine.push_back(0);
     else if (sh->rank >= 0) mine.push_back(sh->rank);
     else for (int r = 0; r < K; ++r) mine.push_back(r);
-    auto shard_psi = [&](int r) { return static_cast<double2 *>(sh ? sh->shards[r] : d->psi); };
+    const bool c64 = d->state_kind == FQ_STATE_C64;
+    auto shard_psi = [&](int r) { return sh ? sh->shards[r] : d->psi; };
+    auto launch = [&](bool ph, bool g, const XyParams &Q, const XyMaps &M, int gr) {
+        return c64 ? launch_xy_any<float>(d->cost_kind, ph, g, Q, M, gr, st)
+                   : launch_xy_any<double>(d->cost_kind, ph, g, Q, M, gr, st);
+    };
     auto shard_costs = [&](int r) { return sh ? sh->costs[r] : d->costs; };
     auto barrier = [&]() -> int {
         if (!sh || sh->rank < 0) return FQ_OK;
@@ -644,7 +668,7 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
                 const long long T = 1LL << (nv - kTileBits);
                 P->nl = nl;
                 for (int r = 0; r < K; ++r) {
-                    P->shard[r] = static_cast<double2 *>(sh->shards[r]);
+                    P->shard[r] = sh->shards[r];
                     P->cshard[r] = sh->costs[r];
                 }
                 P->psi = P->shard[0];
@@ -667,12 +691,7 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
                 XyMaps M;
                 std::memset(&M, 0, sizeof M);
                 const int ggrid = (int)std::min<long long>(P->n_tiles, (long long)sms * 2);
-                int s;
-                if (d->cost_kind == FQ_COST_U16)
-                    s = ph ? launch_xy<FQ_COST_U16, 1, true>(*P, M, ggrid, st) : launch_xy<FQ_COST_U16, 0, true>(*P, M, ggrid, st);
-                else
-                    s = ph ? launch_xy<FQ_COST_F64, 1, true>(*P, M, ggrid, st) : launch_xy<FQ_COST_F64, 0, true>(*P, M, ggrid, st);
-                if (s) return fail(s);
+                if (int s = launch(ph, true, *P, M, ggrid)) return fail(s);
                 launches = ggrid;
                 if (int s2 = barrier()) return fail(s2);
             } else {
@@ -686,8 +705,10 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
                     // tensor prefetch of the next tile (XY passes, unlike the X passes, gain from it at
                     // 128-B runs too: 2.22 vs 2.32 ms per ring layer at n = 26)
                     P->pf = g_xy_prefetch >= 0 ? g_xy_prefetch : ((16 << run_bits_of(pl.tile)) >= 256 ? 1 : 0);
-                    P->sm_rank = cached_tile_map(&M.state, P->psi, nl, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 2,
-                                                P->sm_shift, P->sm_bits);
+                    P->sm_rank = c64 ? cached_tile_map(&M.state, P->psi, nl, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                                       4, 2, P->sm_shift, P->sm_bits)
+                                     : cached_tile_map(&M.state, P->psi, nl, P->tile_pos, CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                                                       8, 2, P->sm_shift, P->sm_bits);
                     P->cm_rank = 0;
                     if (ph || P->expect)
                         P->cm_rank = d->cost_kind == FQ_COST_F64
@@ -695,12 +716,7 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
                                                           CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, 1, P->cm_shift, P->cm_bits)
                                          : cached_tile_map(&M.cost, P->costs, nl, P->tile_pos,
                                                           CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, 1, P->cm_shift, P->cm_bits);
-                    int s;
-                    if (d->cost_kind == FQ_COST_U16)
-                        s = ph ? launch_xy<FQ_COST_U16, 1>(*P, M, grid, st) : launch_xy<FQ_COST_U16, 0>(*P, M, grid, st);
-                    else
-                        s = ph ? launch_xy<FQ_COST_F64, 1>(*P, M, grid, st) : launch_xy<FQ_COST_F64, 0>(*P, M, grid, st);
-                    if (s) return fail(s);
+                    if (int s = launch(ph, false, *P, M, grid)) return fail(s);
                     launches += grid;
                 }
             }
@@ -713,15 +729,18 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
     delete P;
     if (init_pending) {  // zero layers
         for (int r : mine)
-            if (int s = fq_init_state(shard_psi(r), size, -1, d->init_amp, 0, st)) return s;
+            if (int s = c64 ? fq_init_state_c64(shard_psi(r), size, -1, d->init_amp, 0, st)
+                            : fq_init_state(shard_psi(r), size, -1, d->init_amp, 0, st))
+                return s;
     }
     if (d->n_layers == 0 && d->expectation_dev) {
+        auto expect = c64 ? fq_expectation_c64 : fq_expectation;
         if (mine.size() == 1)
-            return fq_expectation(shard_psi(mine[0]), shard_costs(mine[0]), d->cost_kind, d->cost_scale, d->cost_offset,
-                                  size, d->expectation_dev, d->scratch, st);
+            return expect(shard_psi(mine[0]), shard_costs(mine[0]), d->cost_kind, d->cost_scale, d->cost_offset, size,
+                          d->expectation_dev, d->scratch, st);
         for (size_t i = 0; i < mine.size(); ++i)
-            if (int s = fq_expectation(shard_psi(mine[i]), shard_costs(mine[i]), d->cost_kind, d->cost_scale,
-                                       d->cost_offset, size, shard_sums + i, d->scratch, st))
+            if (int s = expect(shard_psi(mine[i]), shard_costs(mine[i]), d->cost_kind, d->cost_scale, d->cost_offset,
+                               size, shard_sums + i, d->scratch, st))
                 return s;
         k_sum_partials<<<1, 32, 0, st>>>(shard_sums, (int)mine.size(), d->expectation_dev);
         FQ_LAUNCHED("k_sum_partials");

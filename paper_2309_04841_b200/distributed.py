@@ -382,8 +382,9 @@ def simulate_qaoa_distributed(problem, params: QaoaParams, K: int, mixer: "str |
     mixer = Mixer.parse(mixer)
     k = _validate_split(n, K)
     dtype = state_dtype(dtype)
-    if dtype == torch.complex64 and not (fused and 1 <= k <= 3 and n - k >= 12 and mixer.kind == "x"):
-        raise ValueError("complex64 sharded states run the fused program: X mixer, K = 2..8, >= 12 qubits per shard")
+    if dtype == torch.complex64 and not (fused and 1 <= k <= 3 and n - k >= 12 and mixer.kind != "custom"):
+        raise ValueError("complex64 sharded states run the fused program: X / XY mixers, K = 2..8, "
+                         ">= 12 qubits per shard")
     state, init = _initial_state(n, mixer, initial, dtype=dtype)
     if init and dtype == torch.complex64:
         init_fn = "fq_init_state_c64"
@@ -451,7 +452,7 @@ class ShardedQaoaSimulator:
                  compact: bool = True, keep_f64: bool | None = None, chunk_bytes: int | None = None,
                  local_ops=None, global_mode: str = "exchange", device_barrier: bool = True, dtype=None):
         """``dtype``: complex128 (default) or complex64 (global_mode="fused",
-        X mixer: half the memory per rank, e.g. n = 35 on two B200s)."""
+        X / XY mixers: half the memory per rank, e.g. n = 35 on two B200s)."""
         self.group = group
         self.dtype = state_dtype(dtype)
         self.K = dist.get_world_size(group)
@@ -460,8 +461,8 @@ class ShardedQaoaSimulator:
         self.k = _validate_split(self.n, self.K)
         self.n_local = self.n - self.k
         self.mixer = Mixer.parse(mixer)
-        if self.dtype == torch.complex64 and (global_mode != "fused" or self.mixer.kind != "x" or self.k == 0):
-            raise ValueError("complex64 sharded states need global_mode='fused', the X mixer and >= 2 ranks")
+        if self.dtype == torch.complex64 and (global_mode != "fused" or self.mixer.kind == "custom" or self.k == 0):
+            raise ValueError("complex64 sharded states need global_mode='fused', the X or XY mixers and >= 2 ranks")
         self.ops = local_ops if local_ops is not None else CudaLocalOps()
         base = self.rank << self.n_local
         if keep_f64 is None:

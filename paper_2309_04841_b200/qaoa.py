@@ -136,7 +136,7 @@ def resolve_costs(problem) -> tuple[DeviceCosts, int]:
 
 def state_dtype(dtype) -> torch.dtype:
     """complex128 (the reference's state, default) or complex64 (optional
-    single-precision state: X mixer only; 1e-4 tolerance)."""
+    single-precision state; 1e-4 tolerance)."""
     if dtype is None:
         return torch.complex128
     if dtype in (torch.complex128, torch.complex64):
@@ -180,8 +180,6 @@ def _initial_state(n: int, mixer: Mixer, initial, out: torch.Tensor | None = Non
 def _evolve(dc: DeviceCosts, n: int, mixer: Mixer, params: QaoaParams, initial,
             out: torch.Tensor | None = None, dtype: torch.dtype = torch.complex128) -> QaoaResult:
     if dtype == torch.complex64:
-        if mixer.preserves_hamming_weight:
-            raise ValueError(f"complex64 states run the X and custom mixers (got {mixer.kind!r}); use complex128")
         if n <= 12:
             # on-chip sizes: the resident fp64 program, rounded to complex64 once at the end
             res = _evolve(dc, n, mixer, params, initial)
@@ -201,8 +199,8 @@ class QaoaSimulator:
     def __init__(self, n: int | None = None, *, terms=None, costs=None, mixer: "str | Mixer" = "x",
                  dtype=None) -> None:
         """``dtype``: state type, complex128 (default, the reference's) or
-        complex64 (optional: half the HBM traffic and memory, X and custom
-        mixers, amplitudes / objective within 1e-4 of complex128)."""
+        complex64 (optional: half the HBM traffic and memory, every mixer,
+        amplitudes / objective within 1e-4 of complex128)."""
         if (terms is None) == (costs is None):
             raise ValueError("pass exactly one of terms= or costs=")
         self.dtype = state_dtype(dtype)
@@ -221,8 +219,6 @@ class QaoaSimulator:
         if n is not None and n != self.n:
             raise ValueError(f"n={n} disagrees with problem size {self.n}")
         self.mixer = Mixer.parse(mixer)
-        if self.dtype == torch.complex64 and self.mixer.preserves_hamming_weight:
-            raise ValueError(f"complex64 states run the X and custom mixers (got {self.mixer.kind!r})")
         self._buffer: torch.Tensor | None = None
 
     @property

@@ -102,15 +102,49 @@ def test_c64_small_n_and_module_functions():
 
 def test_c64_limits():
     with pytest.raises(ValueError):
-        QaoaSimulator(terms=labs_terms(14), mixer="xy-ring", dtype="complex64")
-    with pytest.raises(ValueError):
         QaoaSimulator(terms=labs_terms(14), dtype="float32")
-    # the ABI refuses what the kernels do not implement, loudly
+    # the ABI refuses what the kernels do not implement, loudly: the per-gate XY path is complex128
     from paper_2309_04841_b200.mixers import run_program
 
     psi = torch.empty(1 << 14, dtype=torch.complex64, device=_lib.device())
-    with pytest.raises(RuntimeError):
-        run_program(psi, 14, "xy-ring", [(0.0, 0.3, 0, 0, 14)])
+    _lib.call("fq_set_option", b"xy_tiled", 0)
+    try:
+        with pytest.raises(RuntimeError):
+            run_program(psi, 14, "xy-ring", [(0.0, 0.3, 0, 0, 14)])
+    finally:
+        _lib.call("fq_set_option", b"xy_tiled", 1)
+
+
+@pytest.mark.parametrize("kind,n", [("xy-ring", 15), ("xy-complete", 14), ("xy-ring", 9)])
+def test_c64_xy_vs_oracle(kind, n):
+    """XY mixers on complex64 states (tiled XY passes with R = float; n <= 12 on chip in fp64)."""
+    from paper_2309_04841_b200 import hamming_weight_state
+    from paper_2309_04841_b200.problems import portfolio_terms
+
+    g, b = (0.3, -0.2), (0.4, 0.9)
+    poly = portfolio_terms(n)
+    sim = QaoaSimulator(terms=poly, mixer=kind, dtype="complex64")
+    init = hamming_weight_state(n, n // 2)
+    res = sim.simulate_qaoa(g, b, initial=init)
+    costs = sim.get_cost_diagonal()
+    ref = O.simulate(costs, g, b, kind, init)
+    _check_state(sim.get_statevector(res), ref)
+    _check_energy(sim.get_expectation(res), O.expectation(ref, costs), costs)
+
+
+@pytest.mark.parametrize("kind,n,K", [("xy-ring", 14, 2), ("xy-complete", 15, 8)])
+def test_c64_sharded_xy_in_process(kind, n, K):
+    from paper_2309_04841_b200 import hamming_weight_state
+    from paper_2309_04841_b200.distributed import simulate_qaoa_distributed
+    from paper_2309_04841_b200.problems import portfolio_terms
+
+    params = QaoaParams((0.3, -0.2), (0.4, 0.9))
+    poly = portfolio_terms(n)
+    init = hamming_weight_state(n, n // 2)
+    res = simulate_qaoa_distributed(poly, params, K, mixer=kind, initial=init, dtype="complex64")
+    costs = res.costs
+    ref = O.simulate(costs, params.gammas, params.betas, kind, init)
+    _check_state(res.statevector(), ref)
 
 
 def test_c64_reuse_buffer_and_determinism():
@@ -158,9 +192,11 @@ def test_c64_sharded_in_process_vs_single(n, K, p):
     _check_state(got, ref)
     np.testing.assert_allclose(got, single.state, rtol=0, atol=1e-6 * np.abs(ref).max())
     _check_energy(res.expectation(), O.expectation(ref, costs), costs)
-    with pytest.raises(ValueError):
-        simulate_qaoa_distributed(poly, params, K, mixer="xy-ring", dtype="complex64",
-                                  initial=np.full(1 << n, 2 ** (-n / 2)))
+    with pytest.raises(ValueError):  # custom mixers are single-GPU for complex64
+        from paper_2309_04841_b200 import SU2, Mixer
+
+        simulate_qaoa_distributed(poly, params, K, mixer=Mixer.custom(lambda beta: [SU2.rx(beta)] * n),
+                                  dtype="complex64")
 
 
 @pytest.mark.parametrize("n", [13, 17])
