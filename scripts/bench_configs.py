@@ -171,6 +171,12 @@ def config4(args):
         ms = gpu_time(lambda: sim.get_expectation(sim.simulate_qaoa(g, b, initial=init_d)), 3, warm=1)
         line = {"config": f"4: portfolio n=26 {kind} p={p}", "gpu_ms_per_layer": ms, "gpu_layers_per_s": 1e3 / ms,
                 "cost_encoding": "uint16" if sim.device_costs.u16 is not None else "float64"}
+        # the optional complex64 state on the same problem (same diagonal)
+        sim64 = QaoaSimulator(costs=sim.device_costs, mixer=Mixer(kind), dtype="complex64")
+        init64 = init_d.to(torch.complex64)
+        line["gpu_ms_per_layer_complex64"] = gpu_time(
+            lambda: sim64.get_expectation(sim64.simulate_qaoa(g, b, initial=init64)), 3, warm=1)
+        del sim64
         if not args.skip_cpu:
             from oracle import oracle as O
 
