@@ -76,6 +76,8 @@ def complete_edges(n: int) -> list[tuple[int, int]]:
 
 def su2_table(layers_us: Sequence[Sequence[SU2]]) -> np.ndarray:
     """[layers][n][4] = (a.re, a.im, b.re, b.im) for the custom-mixer kernels."""
+    if len(layers_us) == 0:
+        return np.zeros((0, 0, 4), dtype=np.float64)
     return np.array([[(complex(u.a).real, complex(u.a).imag, complex(u.b).real, complex(u.b).imag) for u in us]
                      for us in layers_us], dtype=np.float64).reshape(len(layers_us), -1, 4)
 
@@ -214,6 +216,8 @@ class Mixer:
             if len(us) != n:
                 raise ValueError(f"expected {n} matrices, got {len(us)}")
             rows.append(us)
+        if not rows:  # zero layers: a (never read) table keeps the descriptor valid
+            return np.zeros((1, n, 4), dtype=np.float64)
         return su2_table(rows)
 
     def apply_layer(self, state, beta: float) -> None:

@@ -298,3 +298,13 @@ def test_device_tensor_inputs():
     ref = O.uniform_state(n)
     O.rx_layer(ref, 0.2)
     np.testing.assert_allclose(psi.cpu().numpy(), ref, atol=1e-13)
+
+
+def test_custom_mixer_zero_layers():
+    """Zero layers under a custom mixer (found by scripts/stress.py): the uniform state."""
+    from paper_2309_04841_b200 import SU2, Mixer
+
+    for n in (5, 14):
+        sim = QaoaSimulator(terms=labs_terms(n), mixer=Mixer.custom(lambda beta: [SU2.rx(beta)] * n))
+        res = sim.simulate_qaoa([], [])
+        np.testing.assert_allclose(res.state, np.full(1 << n, 2 ** (-n / 2)), rtol=0, atol=1e-15)
