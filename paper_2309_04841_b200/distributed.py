@@ -746,6 +746,18 @@ class ShardedQaoaSimulator:
         dist.all_reduce(local, op=dist.ReduceOp.SUM, group=self.group)
         return float(local.item())
 
+    def statevector(self) -> np.ndarray:
+        """The full state on every rank (the reference's DistributedResult.statevector
+        = gather of the shards, distributed.py:267-268); only for sizes that fit
+        one host.  Collective: every rank must call it."""
+        t = self._state
+        if t.is_cuda and dist.get_backend(self.group) == "gloo":
+            t = t.cpu()
+        t = t.contiguous()
+        parts = [torch.empty_like(t) for _ in range(self.K)]
+        dist.all_gather(parts, t, group=self.group)
+        return torch.cat(parts).cpu().numpy()
+
     def overlap(self, tol: float = 0.0) -> float:
         lo = self.ops.min_cost(self.costs)
         dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=self.group)

@@ -90,10 +90,8 @@ def _worker(rank, world, port, n, p, chunk, q):
         instrumentation.reset()
         E = sim.simulate_qaoa(g, b)
         ov = sim.overlap()
-        shards = [torch.empty_like(sim.shard) for _ in range(world)]
-        dist.all_gather(shards, sim.shard)
-        q.put((rank, E, ov, sim.exchange_count, instrumentation.get("exchange"),
-               torch.cat(shards).numpy() if rank == 0 else None))
+        full = sim.statevector()  # gather of the shards on every rank
+        q.put((rank, E, ov, sim.exchange_count, instrumentation.get("exchange"), full if rank == 0 else None))
     finally:
         dist.destroy_process_group()
 
