@@ -50,6 +50,9 @@ def _worker(rank, world, port, n, p, kind, chunk, q, mode="exchange", dev_barrie
                                    device_barrier=dev_barrier, dtype=dtype)
         E = sim.simulate_qaoa(g, b, initial_weight=n // 2 if kind.startswith("xy") else None)
         ov = sim.overlap()
+        full = sim.statevector()  # collective gather; must agree with the shards
+        lo = rank << (n - (world.bit_length() - 1))
+        assert np.array_equal(full[lo:lo + sim.shard.numel()], sim.shard.cpu().numpy())
         q.put((rank, E, ov, sim.exchange_count, sim.shard.cpu().numpy()))
         if mode in ("p2p", "fused"):
             dist.barrier()
