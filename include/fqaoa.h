@@ -223,8 +223,8 @@ typedef struct fq_shard_desc {
     int rank;                       /* this process's shard; -1: all K shards are this
                                        process's (one device, one stream: the reference's
                                        in-process worker model)                            */
-    void *const *shards;            /* [K] complex128 state shards as mapped in this process
-                                       (peers via fq_ipc_open)                               */
+    void *const *shards;            /* [K] state shards (desc->state_kind) as mapped in this
+                                       process (peers via fq_ipc_open)                       */
     const void *const *costs;       /* [K] cost shards, one encoding / scale / offset        */
     void *const *flags;             /* [K] peer flag arrays of fq_peer_barrier (rank >= 0)   */
     unsigned *epoch;                /* host: last barrier epoch used; advanced by the call   */
@@ -247,7 +247,8 @@ typedef struct fq_shard_desc {
  * XY mixers: the tiled XY plan over all n qubits; a pass whose tile holds
  * global qubits spans the shards it covers, each rank taking the tiles of its
  * own shard set (replaces the reference's park-and-exchange per global pair,
- * distributed.py:160-207).  complex128, n_local >= 12. */
+ * distributed.py:160-207).  complex128 (any mixer) or complex64 (X / XY),
+ * n_local >= 12. */
 int fq_qaoa_evolve_sharded(const fq_evolve_desc *desc, const fq_shard_desc *shards, void *stream);
 
 /* Pass count of fq_qaoa_evolve_sharded's plan and, in *global_passes, how many
