@@ -321,7 +321,7 @@ def main():
         gp = ctypes.c_int()
         passes = _lib.load().fq_plan_sharded_passes(n_local, k, p, glay, ctypes.byref(gp))
         tile_bytes = passes * 2 * S - S + (n_phase + 1) * Cb
-        launches = passes + 2 * gp.value + 1  # + two device barriers per spanning pass
+        launches = passes + 2 * gp.value + 2  # + two device barriers per spanning pass, + the expectation (2)
         nvlink_bytes = gp.value * 2 * S * (world - 1) // world
     else:
         post = p * (1 if k > 0 else 0)  # the k-position pass after each exchange
