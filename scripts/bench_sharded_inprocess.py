@@ -45,6 +45,9 @@ def main():
     out["single_ms"] = timed(lambda: E.setdefault("single", simulate_qaoa(poly, params)), args.steps)
     for K in (2, 4, 8):
         out[f"K{K}_ms"] = timed(lambda: D.simulate_qaoa_distributed(poly, params, K), args.steps)
+        # the reference's structure: per layer local passes, exchange, k-position pass, exchange
+        out[f"K{K}_exchange_ms"] = timed(lambda: D.simulate_qaoa_distributed(poly, params, K, fused=False),
+                                         max(1, args.steps // 2))
     r = D.simulate_qaoa_distributed(poly, params, 8)
     out["objective_K8"] = r.expectation()
     out["objective_single"] = sim.get_expectation(sim.simulate_qaoa(params.gammas, params.betas))
