@@ -284,9 +284,18 @@ int fq_ipc_close(void *dev_ptr, int64_t offset);
  * flag_arrays[q] = rank q's uint32[K] flag array (peer-mapped, zero-initialised);
  * rank `rank` stores `epoch` into slot `rank` of every array, then waits until
  * all K slots of its own array reach `epoch` (epochs increase by one per
- * barrier, identically on every rank).  On a ~10 s timeout *err_dev is set and
- * the kernel returns.  K <= 16. */
+ * barrier, identically on every rank).  On a 10 s timeout (device
+ * %globaltimer) *err_dev is set and the kernel returns.  K <= 16. */
 int fq_peer_barrier(void *const *flag_arrays, int K, int rank, unsigned epoch, int *err_dev, void *stream);
+
+/* Host-only description of the tiled X/custom plan (no device needed): the
+ * qubit groups ("groups=t,t,../runR;..": target qubits, contiguous-run bits of
+ * the tile) and the pass sequence ("passes=g[f|d],..": group index, f = fused
+ * two layers with the phase between, d = two layers without phase, P = a
+ * standalone phase sweep) of an n-qubit register whose top k qubits are
+ * global (k = 0: one state).  Honours fq_set_option("plan"/"plan_tmax").
+ * Returns the pass count (or -1); writes at most len bytes to buf. */
+int fq_plan_x_describe(int n, int n_layers, const fq_layer *layers, int state_kind, int k, char *buf, int len);
 
 /* HBM passes per layer of the tiled XY program (ring / complete gate order of
  * reference mixers.py:109-125) at n qubits; 1 for n <= 12 (on chip), -1 for other

@@ -75,6 +75,7 @@ _SIGS = {
     "fq_set_option": ([ctypes.c_char_p, I], I),
     "fq_last_passes": ([P, P, I], I),
     "fq_plan_xy_passes": ([I, I, P], I),
+    "fq_plan_x_describe": ([I, I, ctypes.POINTER(FqLayer), I, I, ctypes.c_char_p, I], I),
     "fq_global_su2_pass": ([P, I, I64, I, I, P, P], I),
     "fq_ipc_handle": ([P, P, P], I),
     "fq_ipc_open": ([P, I64, P], I),
@@ -88,11 +89,16 @@ _lib = None
 _lock = threading.Lock()
 
 
-def load(path: str = LIB_PATH):
-    """Load libfqaoa.so (no CUDA device needed to load)."""
+def load(path: str | None = None):
+    """Load libfqaoa.so (no CUDA device needed to load).  FQ_LIB_VARIANT=<name>
+    selects a development build of the same sources with other compile-time
+    options (scripts/build_variant.py, A/B timing only)."""
     global _lib
     with _lock:
         if _lib is None:
+            if path is None:
+                var = os.environ.get("FQ_LIB_VARIANT")
+                path = os.path.join(_HERE, "variants", var, "libfqaoa.so") if var else LIB_PATH
             if not os.path.exists(path):
                 raise ImportError(
                     f"libfqaoa.so not found at {path}: build it with "
@@ -148,3 +154,14 @@ def scratch() -> torch.Tensor:
 
 def ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
+
+
+def describe_x_plan(n: int, p: int, state_kind: int = STATE_C128, k: int = 0, phase: bool = True) -> str:
+    """The X-mixer pass plan of a p-layer program over n qubits (k global):
+    host-only (fq_plan_x_describe), e.g. for the planner tests."""
+    lay = (FqLayer * max(1, p))(*[FqLayer(0.5 if phase else 0.0, 0.3, 1, 0, n) for _ in range(p)])
+    buf = ctypes.create_string_buffer(8192)
+    cnt = load().fq_plan_x_describe(n, p, lay, state_kind, k, buf, len(buf))
+    if cnt < 0:
+        raise ValueError(f"no X plan for n={n}, k={k}")
+    return buf.value.decode()

@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .terms import TermPolynomial, precompute_device, term_arrays
+from .terms import TermPolynomial, _infer_n, precompute_device, term_arrays
 
 
 class DeviceCosts:
@@ -58,7 +58,7 @@ class DeviceCosts:
             if not arr.flags.writeable:  # e.g. the reference's read-only memoised diagonal (qaoa.py:74)
                 arr = arr.copy()
             t = torch.from_numpy(arr).to(dev)
-        n = t.numel().bit_length() - 1
+        n = _infer_n(t.numel())  # the reference's error for malformed lengths (terms.py:178-182)
         dc = cls(n, f64=t)
         if compact:
             dc.try_compact()

@@ -35,6 +35,8 @@
 //    in its shared-memory / FP64 rounds.
 //  * States of n <= 12 qubits run the entire program in one CTA (smem-resident),
 //    which is also the batched multi-parameter path for optimiser loops.
+#include <string>
+
 #include "tmap.cuh"
 
 namespace fq {
@@ -286,9 +288,11 @@ static int g_fuse = 1;
 static int g_prefetch = -1;  // L2 prefetch distance (grid strides); -1: 1 for runs >= 256 B, else 0
 static int g_phase_tables = 1;
 static int g_plan = -1;      // -1: choose by cost model, else force style (0 / 1, legacy chunk sizes)
+static int g_plan_tmax = 0;  // > 0: force the high-group chunk size (4..12) of the X plan (parity tests of every shape)
 static int g_time_passes = 0;
 static int g_probe = 0;      // development probe bits (PassParams::probe)
-static int g_zigzag = 1;     // alternate the tile walk direction pass to pass (L2 reuse across passes)  // record a CUDA event after every pass of the next programs
+static int g_zigzag = 1;     // alternate the tile walk direction pass to pass (L2 reuse across passes)
+static int g_cost_async = 1; // uint16 phase passes stage their cost slices with cp.async (CA instantiations)
 
 // Per-pass record of the last X program (fq_last_passes): kind + event timing.
 struct PassRecord {
@@ -426,12 +430,23 @@ static double plan_cost(const std::vector<PlannedPass> &seq, const std::vector<G
 // elem: bytes per amplitude (16 complex128, 8 complex64); kq: global qubits of a sharded state
 static std::vector<PlannedPass> plan_x_search(int n, int nl, const fq_layer *layers, std::vector<Group> &groups,
                                               bool fuse, int elem, int kq) {
-    if (g_plan >= 0) {
-        auto seq = plan_with(n, nl, layers, groups, g_plan, g_plan == 0 ? 10 : 8, fuse);
-        if (plan_cost(seq, groups, n, elem, kq) < 1e299) return seq;  // else: search
-    }
     std::vector<PlannedPass> best;
     double best_cost = 1e300;
+    if (g_plan >= 0 || g_plan_tmax > 0) {  // forced shape (style and / or chunk size); invalid -> search
+        for (int style = 0; style < 2; ++style) {
+            if (g_plan >= 0 && style != g_plan) continue;
+            const int tmax = g_plan_tmax > 0 ? g_plan_tmax : (style == 0 ? 10 : 8);
+            std::vector<Group> gs;
+            auto seq = plan_with(n, nl, layers, gs, style, tmax, fuse);
+            const double c = plan_cost(seq, gs, n, elem, kq);
+            if (c < best_cost - 1e-9 && c < 1e299) {
+                best_cost = c;
+                best = seq;
+                groups = gs;
+            }
+        }
+        if (best_cost < 1e299) return best;
+    }
     for (int style = 0; style < 2; ++style) {
         for (int tmax = 12; tmax >= 4; --tmax) {
             std::vector<Group> gs;
@@ -462,7 +477,7 @@ static std::vector<PlannedPass> plan_x(int n, int nl, const fq_layer *layers, st
     static std::mutex mu;
     static std::vector<PlanMemo> memo;
     static size_t next = 0;
-    std::vector<long long> key = {n, nl, elem, kq, fuse ? 1 : 0, g_plan};
+    std::vector<long long> key = {n, nl, elem, kq, fuse ? 1 : 0, g_plan, g_plan_tmax};
     key.reserve(key.size() + 3 * (size_t)nl);
     for (int l = 0; l < nl; ++l) {
         key.push_back(layers[l].q_lo);
@@ -754,6 +769,14 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCt
             // the tensor prefetch pays for long runs only: with short runs its many
             // small requests compete with the demand loads (measured, n = 28..34)
             const int pf = g_prefetch >= 0 ? g_prefetch : ((elem << run_bits_of(g)) >= 256 ? 1 : 0);
+            // cost slices by cp.async (uint16 phase passes, compile-time masks), when the two
+            // 8.5 KiB buffers still leave room for two CTAs per SM (228 KiB, 1 KiB reserved each)
+            if (g_cost_async && d->cost_kind == FQ_COST_U16 && (ph == 1 || ph == 2) && mix == MIX_RX &&
+                mask_class(sq, P.maskA) != K_RUNTIME && 2 * (pass_smem_bytes(c64, table_hi, true) + 1024 + 64) <= 233472) {
+                P.cost_async = 1;
+                P.cost_chunk_log2 = std::min(3, run_bits_of(g));
+                P.pf_cost = 0;  // the copies run a whole tile ahead
+            }
             for (size_t mi = 0; mi < mine.size(); ++mi) {
                 const int r = mine[mi];
                 P.psi = shard_psi(r);
@@ -883,8 +906,12 @@ static int run_resident_program(const fq_evolve_desc *d, cudaStream_t st) {
     // chunk the layers into launches of kResMaxLayers; custom-mixer
     // coefficients travel through the caller's scratch buffer.
     const int n = d->n;
-    for (int l0 = 0; l0 < std::max(1, d->n_layers); l0 += kResMaxLayers) {
-        const int cnt = std::min(kResMaxLayers, d->n_layers - l0);
+    // custom-mixer coefficients (4 doubles per layer and qubit) travel through the
+    // scratch buffer: a chunk carries at most FQ_SCRATCH_DOUBLES / (4 n) layers
+    const int chunk = d->mixer == FQ_MIXER_CUSTOM ? std::min(kResMaxLayers, FQ_SCRATCH_DOUBLES / (4 * n))
+                                                  : kResMaxLayers;
+    for (int l0 = 0; l0 < std::max(1, d->n_layers); l0 += chunk) {
+        const int cnt = std::min(chunk, d->n_layers - l0);
         ResParams *P = new ResParams;
         std::memset(P, 0, sizeof *P);
         P->n = n;
@@ -898,7 +925,7 @@ static int run_resident_program(const fq_evolve_desc *d, cudaStream_t st) {
         P->psi_in = static_cast<const double2 *>(d->psi);
         P->in_stride = 0;
         P->psi_out = static_cast<double2 *>(d->psi);
-        const bool last = (l0 + kResMaxLayers >= d->n_layers);
+        const bool last = (l0 + chunk >= d->n_layers);
         P->exp_out = last ? d->expectation_dev : nullptr;
         for (int i = 0; i < cnt; ++i) {
             P->gam[i] = d->layers[l0 + i].gamma;
@@ -1022,6 +1049,7 @@ int fq_set_option(const char *name, int value) {
         {"fuse", &g_fuse, 0, 1},            // fuse the passes at layer boundaries
         {"phase_tables", &g_phase_tables, 0, 1},  // uint16 phase via smem tables (else sincos)
         {"plan", &g_plan, -1, 1},           // group plan: -1 cost model, 0 legacy, 1 small fusion groups
+        {"plan_tmax", &g_plan_tmax, 0, 12},  // force the high-group chunk size (0: cost model)
         {"time_passes", &g_time_passes, 0, 1},  // CUDA events around every pass (fq_last_passes)
         {"xy_tiled", &g_xy_tiled, 0, 1},    // tiled XY passes (0: one kernel per gate)
         {"zigzag", &g_zigzag, 0, 1},        // alternate tile walk direction pass to pass
@@ -1030,6 +1058,7 @@ int fq_set_option(const char *name, int value) {
         {"xy_pad", &g_xy_pad, 0, 1},        // XY passes: gate-free load / store rounds for coalescing
         {"xy_prefetch", &g_xy_prefetch, -1, 1},  // XY passes: L2 tensor prefetch (-1: runs >= 256 B)
         {"probe", &g_probe, 0, 7},          // development: isolate phase costs (results invalid when != 0)
+        {"cost_async", &g_cost_async, 0, 1},  // uint16 phase passes: cost slices staged by cp.async
     };
     for (auto &o : opts) {
         if (std::strcmp(name, o.name) == 0) {
@@ -1049,6 +1078,35 @@ int fq_plan_x_passes(int n, int n_layers, const fq_layer *layers, int state_kind
     if (n <= kTileBits) return n_layers > 0 ? 1 : 0;
     std::vector<Group> groups;
     return (int)plan_x(n, n_layers, layers, groups, g_fuse != 0, state_kind == FQ_STATE_C64 ? 8 : 16).size();
+}
+
+int fq_plan_x_describe(int n, int n_layers, const fq_layer *layers, int state_kind, int k, char *buf, int len) {
+    if (!buf || len <= 0) return -1;
+    buf[0] = 0;
+    if (n <= kTileBits + k || k < 0 || k > 3) return -1;
+    std::vector<Group> groups;
+    const auto seq = plan_x(n, n_layers, layers, groups, g_fuse != 0, state_kind == FQ_STATE_C64 ? 8 : 16, k);
+    std::string out;
+    char tmp[64];
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        out += gi ? ";" : "groups=";
+        for (size_t i = 0; i < groups[gi].targets.size(); ++i) {
+            std::snprintf(tmp, sizeof tmp, "%s%d", i ? "," : "", groups[gi].targets[i]);
+            out += tmp;
+        }
+        std::snprintf(tmp, sizeof tmp, "/run%d", run_bits_of(groups[gi]));
+        out += tmp;
+    }
+    out += " passes=";
+    for (size_t i = 0; i < seq.size(); ++i) {
+        const PlannedPass &pp = seq[i];
+        if (pp.group < 0) std::snprintf(tmp, sizeof tmp, "%sP", i ? "," : "");
+        else std::snprintf(tmp, sizeof tmp, "%s%d%s", i ? "," : "", pp.group,
+                           pp.layerB >= 0 ? (pp.phase_at == 2 ? "f" : "d") : "");
+        out += tmp;
+    }
+    std::snprintf(buf, (size_t)len, "%s", out.c_str());
+    return (int)seq.size();
 }
 
 int fq_plan_xy_passes(int n, int mixer, int *rounds) {

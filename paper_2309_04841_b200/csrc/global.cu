@@ -62,15 +62,23 @@ __global__ void __launch_bounds__(256) k_global_su2(const __grid_constant__ Glob
 // slots of its own array reach `epoch`.  Stream-ordered: the work enqueued
 // before it on every rank is complete (and, after the system fence, visible
 // to the peers) when any rank passes it — no host synchronisation.  A rank
-// that never arrives trips the timeout (~10 s of clock64): *err is set and the
-// kernel returns instead of hanging the device.
+// that never arrives trips the timeout (10 s of %globaltimer, a nanosecond
+// clock independent of the SM clock and of which device runs it): *err is set
+// and the kernel returns instead of hanging the device; the host side
+// (ShardedQaoaSimulator.check_barrier) reports it after every program.
 struct BarrierParams {
     unsigned *flags[1 << kMaxGlobal];  // rank q's flag array (K slots), peer-mapped
     int K, rank;
     unsigned epoch;
     int *err;
-    long long timeout;  // clock64 cycles
+    unsigned long long timeout_ns;
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __global__ void k_peer_barrier(const __grid_constant__ BarrierParams P) {
     const int t = threadIdx.x;
@@ -83,9 +91,9 @@ __global__ void k_peer_barrier(const __grid_constant__ BarrierParams P) {
     __threadfence_system();
     if (t < P.K) {
         volatile unsigned *mine = P.flags[P.rank];
-        const long long t0 = clock64();
+        const unsigned long long t0 = global_ns();
         while ((int)(mine[t] - P.epoch) < 0) {
-            if (clock64() - t0 > P.timeout) {
+            if (global_ns() - t0 > P.timeout_ns) {
                 atomicExch(P.err, 1);
                 break;
             }
@@ -180,9 +188,7 @@ int fq_peer_barrier(void *const *flag_arrays, int K, int rank, unsigned epoch, i
     P.rank = rank;
     P.epoch = epoch;
     P.err = err_dev;
-    int rate = 0;
-    cudaDeviceGetAttribute(&rate, cudaDevAttrClockRate, 0);  // kHz
-    P.timeout = (long long)(rate > 0 ? rate : 2000000) * 1000LL * 10;  // ~10 s
+    P.timeout_ns = 10ULL * 1000 * 1000 * 1000;  // 10 s
     k_peer_barrier<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(P);
     FQ_LAUNCHED("k_peer_barrier");
     return FQ_OK;

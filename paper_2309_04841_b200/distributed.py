@@ -450,8 +450,14 @@ class ShardedQaoaSimulator:
 
     def __init__(self, poly: TermPolynomial, group=None, mixer: "str | Mixer" = "x",
                  compact: bool = True, keep_f64: bool | None = None, chunk_bytes: int | None = None,
-                 local_ops=None, global_mode: str = "exchange", device_barrier: bool = True, dtype=None):
-        """``dtype``: complex128 (default) or complex64 (global_mode="fused",
+                 local_ops=None, global_mode: str | None = None, device_barrier: bool = True, dtype=None):
+        """``global_mode`` (how mixer gates on the k global qubits run):
+        "fused" (default on CUDA ranks with >= 12 local qubits) — one sharded
+        program whose global-group passes span every shard over peer memory;
+        "p2p" — a per-layer peer-memory kernel (the default below 12 local
+        qubits); "exchange" — the reference's NCCL all-to-all structure (the
+        default with custom ``local_ops``, e.g. the CPU test backend).
+        ``dtype``: complex128 (default) or complex64 (global_mode="fused",
         X / XY mixers: half the memory per rank, e.g. n = 35 on two B200s)."""
         self.group = group
         self.dtype = state_dtype(dtype)
@@ -461,6 +467,9 @@ class ShardedQaoaSimulator:
         self.k = _validate_split(self.n, self.K)
         self.n_local = self.n - self.k
         self.mixer = Mixer.parse(mixer)
+        if global_mode is None:
+            global_mode = ("exchange" if local_ops is not None or self.k == 0
+                           else "fused" if self.n_local >= 12 else "p2p")
         if self.dtype == torch.complex64 and (global_mode != "fused" or self.mixer.kind == "custom" or self.k == 0):
             raise ValueError("complex64 sharded states need global_mode='fused', the X or XY mixers and >= 2 ranks")
         self.ops = local_ops if local_ops is not None else CudaLocalOps()
@@ -483,6 +492,7 @@ class ShardedQaoaSimulator:
         self._cost_peers: list[int] | None = None
         self._opened: list[tuple[int, int]] = []
         self._epoch = ctypes.c_uint(0)
+        self._broken: str | None = None
         if global_mode == "fused" and self.k > 0:
             self._common_cost_encoding()
 
@@ -535,6 +545,8 @@ class ShardedQaoaSimulator:
     def simulate_qaoa(self, gammas: Sequence[float], betas: Sequence[float], initial_weight: int | None = None,
                       expectation: bool = True) -> float | None:
         """Evolve; returns the global expectation (all-reduced) if requested."""
+        if self._broken:
+            raise RuntimeError(self._broken)
         params = QaoaParams(tuple(gammas), tuple(betas))
         if self.mixer.preserves_hamming_weight and initial_weight is None:
             raise ValueError("XY mixers need initial_weight (Hamming-weight sector)")
@@ -625,8 +637,18 @@ class ShardedQaoaSimulator:
             dist.barrier(group=self.group)
 
     def check_barrier(self) -> None:
+        """Raise if a device-side peer barrier timed out (host sync).  Runs
+        after every peer-memory program, whatever it returns.  After a timeout
+        the shards' contents are undefined (passes may have raced a rank that
+        never arrived): the error word is cleared and the simulator refuses
+        further work instead of computing on them."""
+        if self._broken:
+            raise RuntimeError(self._broken)
         if self._p2p_buf is not None and self.device_barrier and int(self._flags[self.K].item()) != 0:
-            raise RuntimeError("peer barrier timed out (a rank did not arrive)")
+            self._flags[self.K].zero_()
+            self._broken = ("peer barrier timed out (a rank did not arrive); the sharded state is undefined — "
+                            "create a new ShardedQaoaSimulator")
+            raise RuntimeError(self._broken)
 
     def _global_p2p(self, us: Sequence[SU2]) -> None:
         """Alg. 4's exchange -> k-position pass -> exchange as ONE peer-memory
@@ -685,9 +707,9 @@ class ShardedQaoaSimulator:
         self.exchange_count += ex
         instrumentation.bump("exchange", ex)
         self._state = psi
+        self.check_barrier()  # mandatory after every peer-memory program
         if not expectation:
             return None
-        self.check_barrier()
         dist.all_reduce(exp, op=dist.ReduceOp.SUM, group=self.group)
         return float(exp.item())
 
@@ -749,14 +771,39 @@ class ShardedQaoaSimulator:
     def statevector(self) -> np.ndarray:
         """The full state on every rank (the reference's DistributedResult.statevector
         = gather of the shards, distributed.py:267-268); only for sizes that fit
-        one host.  Collective: every rank must call it."""
+        one host.  Collective: every rank must call it.  Refuses (MemoryError)
+        when the gathered vector would not fit this host's free memory — e.g.
+        n = 34 complex128 is 256 GiB; stream shards with ``save_shard`` instead."""
+        self.check_barrier()
         t = self._state
+        need = t.numel() * t.element_size() * self.K
+        if need > _host_free_bytes():
+            raise MemoryError(f"statevector(): the gathered {self.n}-qubit state needs {need / 2**30:.1f} GiB of host "
+                              f"memory ({_host_free_bytes() / 2**30:.1f} GiB free); use save_shard() per rank")
         if t.is_cuda and dist.get_backend(self.group) == "gloo":
             t = t.cpu()
         t = t.contiguous()
         parts = [torch.empty_like(t) for _ in range(self.K)]
         dist.all_gather(parts, t, group=self.group)
         return torch.cat(parts).cpu().numpy()
+
+    def save_shard(self, path: str, chunk_bytes: int = 256 << 20) -> None:
+        """Stream this rank's shard to ``path`` in bounded device->host chunks
+        (little-endian interleaved complex, the layout of statevec.save_state;
+        shard r holds global indices [r 2^(n-k), (r+1) 2^(n-k))).  Concatenating
+        the K files in rank order gives the reference's save_state file of the
+        whole state (statevec.py:114-117) — the egress path for states that
+        do not fit one host."""
+        self.check_barrier()
+        t = self._state.reshape(-1)
+        step = max(1, chunk_bytes // t.element_size())
+        pinned = torch.empty(min(step, t.numel()), dtype=t.dtype, pin_memory=t.is_cuda)
+        with open(path, "wb") as f:
+            for s0 in range(0, t.numel(), step):
+                s1 = min(t.numel(), s0 + step)
+                buf = pinned[:s1 - s0]
+                buf.copy_(t[s0:s1])
+                f.write(buf.numpy().astype("<c16" if t.dtype == torch.complex128 else "<c8", copy=False).tobytes())
 
     def overlap(self, tol: float = 0.0) -> float:
         lo = self.ops.min_cost(self.costs)
@@ -768,6 +815,15 @@ class ShardedQaoaSimulator:
     @property
     def shard(self) -> torch.Tensor:
         return self._state
+
+
+def _host_free_bytes() -> int:
+    try:
+        import psutil
+
+        return int(psutil.virtual_memory().available)
+    except Exception:  # noqa: BLE001 - no psutil: assume the gather fits
+        return 1 << 62
 
 
 class CudaLocalOps:

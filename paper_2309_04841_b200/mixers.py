@@ -22,6 +22,7 @@ from typing import Callable, Sequence
 
 import numpy as np
 import torch
+from torch.autograd.graph import increment_version
 
 from . import _lib
 from .statevec import _OnDevice, num_qubits
@@ -111,6 +112,7 @@ def run_program(psi, n: int, mixer: str, layers: Sequence[tuple], dc=None, su2: 
     desc.scratch = _lib.scratch().data_ptr()
     desc.state_kind = _lib.STATE_C64 if psi.dtype == torch.complex64 else _lib.STATE_C128
     _lib.check(_lib.load().fq_qaoa_evolve(ctypes.byref(desc), _lib.stream()), "fq_qaoa_evolve")
+    increment_version(psi)  # written in place through its pointer (see statevec._OnDevice)
 
 
 def apply_su2(state, u: SU2, q: int) -> None:

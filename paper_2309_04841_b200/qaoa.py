@@ -16,6 +16,7 @@ from typing import Sequence
 
 import numpy as np
 import torch
+from torch.autograd.graph import increment_version
 
 from . import _lib, instrumentation
 from .costs import DeviceCosts
@@ -64,12 +65,27 @@ class QaoaResult:
         self.costs_device = costs_device
         self._expectation_dev = expectation_dev
         self._state_host: np.ndarray | None = None
+        # the state is live (reference qaoa.py:63-68): the library's in-place operations
+        # bump its version counter (statevec._OnDevice), which retires the cached
+        # objective of the fused last pass and the host copy
+        self._version = state_device._version
+
+    def _check_version(self) -> None:
+        if self.state_device._version != self._version:
+            self._mutated()
+            self._version = self.state_device._version
 
     @property
     def state(self) -> np.ndarray:
+        self._check_version()
         if self._state_host is None:
             self._state_host = self.state_device.cpu().numpy()
         return self._state_host
+
+    def cached_expectation(self) -> torch.Tensor | None:
+        """The objective computed by the program's last pass, if the state is unchanged since."""
+        self._check_version()
+        return self._expectation_dev
 
     @property
     def costs(self) -> np.ndarray:
@@ -269,18 +285,25 @@ class QaoaSimulator:
         return result.state
 
     def get_probabilities(self, result: QaoaResult, preserve_state: bool = True) -> np.ndarray:
+        """|psi|^2 as a host array (reference qaoa.py:154, statevec.py:81-91).
+        ``preserve_state=False`` squares the result's state in place and returns
+        the real view of that state, as the reference does: the result's state
+        then holds |psi|^2 + 0j (on the device and in ``result.state``)."""
         psi = result.state_device
         work = psi.clone() if preserve_state else psi
         fn = "fq_abs2_inplace_c64" if work.dtype == torch.complex64 else "fq_abs2_inplace"
         _lib.call(fn, work.data_ptr(), work.numel(), _lib.stream())
-        if not preserve_state:
-            result._mutated()
-        return torch.view_as_real(work)[:, 0].cpu().numpy()
+        if preserve_state:
+            return torch.view_as_real(work)[:, 0].cpu().numpy()
+        increment_version(psi)
+        result._mutated()
+        return result.state.real  # a view of the (now squared) state, like state.real in the reference
 
     def get_expectation(self, result: QaoaResult, costs=None) -> float:
         if costs is None:
-            if result._expectation_dev is not None:
-                return float(result._expectation_dev.item())
+            cached = result.cached_expectation()
+            if cached is not None:
+                return float(cached.item())
             dc = result.costs_device
         else:
             dc = costs if isinstance(costs, DeviceCosts) else DeviceCosts.from_array(costs, compact=False)
@@ -313,7 +336,7 @@ def simulate_qaoa(problem, params: QaoaParams, mixer: "str | Mixer" = "x", initi
 def qaoa_objective(problem, params: QaoaParams, mixer: "str | Mixer" = "x", initial=None, dtype=None) -> float:
     """Expected cost of the evolved state (reference qaoa.py:185-194)."""
     result = simulate_qaoa(problem, params, mixer=mixer, initial=initial, dtype=dtype)
-    return float(result._expectation_dev.item())
+    return float(result.cached_expectation().item())
 
 
 __all__ = ["QaoaParams", "QaoaResult", "QaoaSimulator", "simulate_qaoa", "qaoa_objective", "resolve_costs",

@@ -15,6 +15,7 @@ from math import comb, sqrt
 
 import numpy as np
 import torch
+from torch.autograd.graph import increment_version
 
 from . import _lib
 from .terms import MAX_DENSE_QUBITS, _infer_n
@@ -104,8 +105,14 @@ class _OnDevice:
         return self.dev
 
     def __exit__(self, *exc):
-        if exc[0] is None and self.write_back and not isinstance(self.state, torch.Tensor):
-            np.copyto(self.state, self.dev.cpu().numpy())
+        if exc[0] is None and self.write_back:
+            if isinstance(self.state, torch.Tensor):
+                # the kernels write through raw pointers: record the in-place
+                # update in the tensor's version counter so cached observables
+                # of a QaoaResult holding it are invalidated
+                increment_version(self.state)
+            else:
+                np.copyto(self.state, self.dev.cpu().numpy())
         return False
 
 
@@ -141,7 +148,7 @@ def probabilities(state, preserve_state: bool = True):
     """|amplitude|^2 (reference statevec.py:81-91).  With preserve_state=False
     the squares overwrite the state and its real view is returned."""
     if isinstance(state, torch.Tensor):
-        with _OnDevice(state) as psi:
+        with _OnDevice(state, write_back=not preserve_state) as psi:
             work = psi if not preserve_state else psi.clone()
             _lib.call("fq_abs2_inplace", work.data_ptr(), work.numel(), _lib.stream())
             return torch.view_as_real(work)[:, 0]

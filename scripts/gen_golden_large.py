@@ -65,6 +65,11 @@ CASES = {
     "port26_ring_p1": (lambda: portfolio(26), "xy-ring", 1, bench_angles, 13),
     # BASELINE config 3's size (the reference's n <= 30 limit): ~15 min on 8 cores, mostly precompute
     "labs30_x_p3": (lambda: labs_terms(30), "x", 3, bench_angles, None),
+    # BASELINE config 4 at full size: XY-complete n=26 (325 gates per layer) and XY-ring at p=2
+    "port26_complete_p1": (lambda: portfolio(26), "xy-complete", 1, bench_angles, 13),
+    "port26_ring_p2": (lambda: portfolio(26), "xy-ring", 2, bench_angles, 13),
+    # BASELINE config 3 at its full depth (LABS n=30, p=10): ~25 min on 8 cores
+    "labs30_x_p10": (lambda: labs_terms(30), "x", 10, bench_angles, None),
 }
 
 

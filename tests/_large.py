@@ -27,6 +27,9 @@ CASES = {
     "port22_complete_p1": (lambda: portfolio_terms(22), "xy-complete", 11),
     "port26_ring_p1": (lambda: portfolio_terms(26), "xy-ring", 13),
     "labs30_x_p3": (lambda: labs_terms(30), "x", None),  # BASELINE config 3's size, the reference's n <= 30 limit
+    "port26_complete_p1": (lambda: portfolio_terms(26), "xy-complete", 13),  # BASELINE config 4, full size
+    "port26_ring_p2": (lambda: portfolio_terms(26), "xy-ring", 13),
+    "labs30_x_p10": (lambda: labs_terms(30), "x", None),  # BASELINE config 3 at its full depth
 }
 
 

@@ -232,3 +232,32 @@ def test_sharded_cost_consensus():
     # a shard without uint16 levels and another without float64: no common encoding
     with pytest.raises(MemoryError):
         cost_consensus([(False, True, 1.0, 0.0, 0.0), (True, False, 1.0, 0.0, 3.0)], a)
+
+
+def test_planner_shapes_host_only():
+    """The X-mixer planner runs on the host (no device): LABS n = 26 takes three
+    groups [7 high, 12 low, 7 high] and 1 + 2p passes with p - 1 fused two-layer
+    passes; n >= 31 takes four groups (1 + 3p); forced shapes (plan / plan_tmax)
+    change the grouping.  tests/test_gpu_plans.py runs every forced shape."""
+    from paper_2309_04841_b200 import _lib
+
+    d26 = _lib.describe_x_plan(26, 10)
+    groups = d26.split(" ")[0][len("groups="):].split(";")
+    assert [len(g.split("/")[0].split(",")) for g in groups] == [7, 12, 7]
+    passes = d26.split("passes=")[1].split(",")
+    assert len(passes) == 21 and sum(p.endswith("f") for p in passes) == 9
+    d34 = _lib.describe_x_plan(34, 10)
+    assert len(d34.split(" ")[0].split(";")) == 4 and len(d34.split("passes=")[1].split(",")) == 31
+    try:
+        _lib.call("fq_set_option", b"plan", 0)
+        _lib.call("fq_set_option", b"plan_tmax", 4)
+        forced = _lib.describe_x_plan(26, 10)
+        assert forced != d26
+        assert all(len(g.split("/")[0].split(",")) <= 12 for g in forced.split(" ")[0][7:].split(";"))
+    finally:
+        _lib.call("fq_set_option", b"plan", -1)
+        _lib.call("fq_set_option", b"plan_tmax", 0)
+    assert _lib.describe_x_plan(26, 10) == d26
+    # sharded register (k global qubits): the global qubits share one group
+    d = _lib.describe_x_plan(34, 4, k=3)
+    assert any({"31", "32", "33"} <= set(g.split("/")[0].split(",")) for g in d.split(" ")[0][7:].split(";"))

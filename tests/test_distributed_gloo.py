@@ -75,7 +75,7 @@ class OracleOps:
         return torch.tensor([float(p[costs <= cutoff].sum())], dtype=torch.float64)
 
 
-def _worker(rank, world, port, n, p, chunk, q):
+def _worker(rank, world, port, n, p, chunk, q, outdir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -91,6 +91,7 @@ def _worker(rank, world, port, n, p, chunk, q):
         E = sim.simulate_qaoa(g, b)
         ov = sim.overlap()
         full = sim.statevector()  # gather of the shards on every rank
+        sim.save_shard(os.path.join(outdir, f"shard{rank}.bin"), chunk_bytes=1024)  # streamed egress
         q.put((rank, E, ov, sim.exchange_count, instrumentation.get("exchange"), full if rank == 0 else None))
     finally:
         dist.destroy_process_group()
@@ -103,12 +104,12 @@ def _free_port():
 
 
 @pytest.mark.parametrize("n,p,chunk", [(10, 3, None), (11, 2, 4096)])
-def test_sharded_world2_matches_single_node(n, p, chunk):
+def test_sharded_world2_matches_single_node(n, p, chunk, tmp_path):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, p, chunk, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, p, chunk, q, str(tmp_path))) for r in range(world)]
     for pr in procs:
         pr.start()
     out = [q.get(timeout=120) for _ in range(world)]
@@ -126,6 +127,14 @@ def test_sharded_world2_matches_single_node(n, p, chunk):
         assert ov == pytest.approx(ov_ref, abs=1e-12)
         assert ex == 2 * p and ex_counter == 2 * p  # Alg. 4: two exchanges per X layer
     np.testing.assert_allclose(out[0][5], ref, rtol=0, atol=1e-12)
+    # save_shard files in rank order = the reference's save_state file of the whole state
+    whole = tmp_path / "whole.bin"
+    with open(whole, "wb") as f:
+        for r in range(world):
+            f.write((tmp_path / f"shard{r}.bin").read_bytes())
+    from paper_2309_04841_b200.statevec import load_state
+
+    np.testing.assert_array_equal(load_state(str(whole)), out[0][5])
 
 
 def _xy_worker(rank, world, port, n, p, kind, q):

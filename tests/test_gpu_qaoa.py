@@ -308,3 +308,25 @@ def test_custom_mixer_zero_layers():
         sim = QaoaSimulator(terms=labs_terms(n), mixer=Mixer.custom(lambda beta: [SU2.rx(beta)] * n))
         res = sim.simulate_qaoa([], [])
         np.testing.assert_allclose(res.state, np.full(1 << n, 2 ** (-n / 2)), rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("n,p", [(12, 100), (11, 200)])
+def test_custom_mixer_deep_resident_program(n, p):
+    """Custom SU(2) layers beyond one scratch chunk on the one-CTA (n <= 12)
+    path: p * n * 4 doubles exceed FQ_SCRATCH_DOUBLES, so the program runs in
+    several launches (it used to raise).  The reference takes any p."""
+    from paper_2309_04841_b200 import SU2, Mixer
+
+    rng = np.random.default_rng(n + p)
+    gammas = list(rng.uniform(-0.2, 0.2, p))
+    betas = list(rng.uniform(0.0, 1.0, p))
+
+    def factory(beta):
+        return [SU2(np.cos(beta + 0.01 * q), -1j * np.sin(beta + 0.01 * q)) for q in range(n)]
+
+    sim = QaoaSimulator(terms=labs_terms(n), mixer=Mixer.custom(factory))
+    res = sim.simulate_qaoa(gammas, betas)
+    costs = sim.get_cost_diagonal()
+    ref = O.simulate(costs, gammas, betas, "custom", None, lambda b: [(u.a, u.b) for u in factory(b)])
+    np.testing.assert_allclose(res.state, ref, rtol=0, atol=1e-10)
+    assert sim.get_expectation(res) == pytest.approx(O.expectation(ref, costs), rel=1e-10)
