@@ -292,7 +292,6 @@ static int g_plan_tmax = 0;  // > 0: force the high-group chunk size (4..12) of 
 static int g_time_passes = 0;
 static int g_probe = 0;      // development probe bits (PassParams::probe)
 static int g_zigzag = 1;     // alternate the tile walk direction pass to pass (L2 reuse across passes)
-static int g_cost_async = 1; // uint16 phase passes stage their cost slices with cp.async (CA instantiations)
 
 // Per-pass record of the last X program (fq_last_passes): kind + event timing.
 struct PassRecord {
@@ -769,14 +768,6 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCt
             // the tensor prefetch pays for long runs only: with short runs its many
             // small requests compete with the demand loads (measured, n = 28..34)
             const int pf = g_prefetch >= 0 ? g_prefetch : ((elem << run_bits_of(g)) >= 256 ? 1 : 0);
-            // cost slices by cp.async (uint16 phase passes, compile-time masks), when the two
-            // 8.5 KiB buffers still leave room for two CTAs per SM (228 KiB, 1 KiB reserved each)
-            if (g_cost_async && d->cost_kind == FQ_COST_U16 && (ph == 1 || ph == 2) && mix == MIX_RX &&
-                mask_class(sq, P.maskA) != K_RUNTIME && 2 * (pass_smem_bytes(c64, table_hi, true) + 1024 + 64) <= 233472) {
-                P.cost_async = 1;
-                P.cost_chunk_log2 = std::min(3, run_bits_of(g));
-                P.pf_cost = 0;  // the copies run a whole tile ahead
-            }
             for (size_t mi = 0; mi < mine.size(); ++mi) {
                 const int r = mine[mi];
                 P.psi = shard_psi(r);
@@ -1058,7 +1049,6 @@ int fq_set_option(const char *name, int value) {
         {"xy_pad", &g_xy_pad, 0, 1},        // XY passes: gate-free load / store rounds for coalescing
         {"xy_prefetch", &g_xy_prefetch, -1, 1},  // XY passes: L2 tensor prefetch (-1: runs >= 256 B)
         {"probe", &g_probe, 0, 7},          // development: isolate phase costs (results invalid when != 0)
-        {"cost_async", &g_cost_async, 0, 1},  // uint16 phase passes: cost slices staged by cp.async
     };
     for (auto &o : opts) {
         if (std::strcmp(name, o.name) == 0) {

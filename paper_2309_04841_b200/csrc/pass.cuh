@@ -83,8 +83,6 @@ struct PassParams {
     int sm_rank, sm_shift[5], sm_bits[5];  // state tensor map: rank, outer-dim coordinate = (t >> shift) & (2^bits - 1)
     int cm_rank, cm_shift[5], cm_bits[5];  // cost tensor map (cm_rank = 0: no cost prefetch)
     int probe;                // development: 1 no cost loads, 2 fixed table row, 4 no phase multiply
-    int cost_async;           // CA instantiation chosen: the phase's cost slices arrive by cp.async
-    int cost_chunk_log2;      // cp.async chunk, log2 elements (min(3, run_bits)); 0: synchronous copies
     long long roff[3][kRegs]; // per pattern: BYTE offset of register i in the state (read from the constant
                               // bank, so no register holds the 16 offsets across the rounds)
     long long coff[3][kRegs]; // the same in the cost vector (bytes)
@@ -119,34 +117,6 @@ __device__ __forceinline__ int tile_bit_of_reg(int j) {
 // so every access is [base register + immediate], and a quarter-warp's eight
 // 16-B accesses always fall in eight distinct bank groups.
 constexpr int kTilePadded = kTile + kTile / 16;
-
-// ---- cost slices staged in shared memory (CA passes)
-// The uint16 cost slice of a tile (8 KiB) is copied with cp.async into one of
-// two shared-memory buffers while the CTA works on the previous tile, so the
-// phase reads its levels from shared memory: no global-load latency on the
-// critical path and no registers held across the first round.  Element e sits
-// at e + 16 (e >> 8): the PAT4 read pattern (lanes 0-15 / 16-31 = elements
-// e, e + 256) then hits disjoint banks.
-constexpr int kCostPadded = kTile + kTile / 16;
-__host__ __device__ constexpr int cost_slot(int e) { return e + ((e >> 8) << 4); }
-
-__device__ __forceinline__ void cp_async_bytes(void *dst, const void *src, int bytes) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-    if (bytes == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(src) : "memory");
-    else if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(src) : "memory");
-    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// tile element e of pattern PAT: thread tid, register i
-template <int PAT>
-__device__ __forceinline__ int pat_elem(int tid, int i) {
-    if (PAT == PAT8) return (tid & 255) | (i << 8);
-    if (PAT == PAT0) return i | ((tid & 255) << 4);
-    return (tid & 15) | (i << 4) | ((tid >> 4) << 8);
-}
 
 template <int PAT>
 __device__ __forceinline__ int pat_base(int tid) {
@@ -213,39 +183,8 @@ __device__ __forceinline__ void bfly_su2(T &x0, T &x1, T a, T b) {
     x1.y = b.x * p.y + b.y * p.x + a.x * q.y - a.y * q.x;
 }
 
-// Two qubits of one Rx layer at once: (a I - i d X) (x) (a I - i d X) on the
-// four amplitudes x0 (00), x1 (01), x2 (10), x3 (11):
-//   y0 = a^2 x0 - i a d (x1 + x2) - d^2 x3,   y3 = a^2 x3 - i a d (x1 + x2) - d^2 x0,
-//   y1 = a^2 x1 - i a d (x0 + x3) - d^2 x2,   y2 = a^2 x2 - i a d (x0 + x3) - d^2 x1.
-// Form 0 (a, d) = (1, t): 4 DADD + 16 DFMA per 4 amplitudes and 2 qubits (1.25 FP64
-// operations per amplitude and qubit instead of 2 for two single-qubit butterflies).
-// Form 1 (a, d) = (u, 1) the same with the roles of the squares swapped.
-template <int M, typename T, typename R>
-__device__ __forceinline__ void bfly_rx_pair(T &x0, T &x1, T &x2, T &x3, R r, R r2) {
-    const T a = x0, b = x1, c = x2, d = x3;
-    const R sx = b.x + c.x, sy = b.y + c.y;  // x1 + x2
-    const R wx = a.x + d.x, wy = a.y + d.y;  // x0 + x3
-    if (M == 0) {  // y = x_self - t^2 x_opp - i t s ;  -i t (s.x + i s.y) = t s.y - i t s.x
-        x0 = Cx<R>::make(fma(r, sy, fma(-r2, d.x, a.x)), fma(-r, sx, fma(-r2, d.y, a.y)));
-        x3 = Cx<R>::make(fma(r, sy, fma(-r2, a.x, d.x)), fma(-r, sx, fma(-r2, a.y, d.y)));
-        x1 = Cx<R>::make(fma(r, wy, fma(-r2, c.x, b.x)), fma(-r, wx, fma(-r2, c.y, b.y)));
-        x2 = Cx<R>::make(fma(r, wy, fma(-r2, b.x, c.x)), fma(-r, wx, fma(-r2, b.y, c.y)));
-    } else {       // y = u^2 x_self - x_opp - i u s
-        x0 = Cx<R>::make(fma(r, sy, fma(r2, a.x, -d.x)), fma(-r, sx, fma(r2, a.y, -d.y)));
-        x3 = Cx<R>::make(fma(r, sy, fma(r2, d.x, -a.x)), fma(-r, sx, fma(r2, d.y, -a.y)));
-        x1 = Cx<R>::make(fma(r, wy, fma(r2, b.x, -c.x)), fma(-r, wx, fma(r2, b.y, -c.y)));
-        x2 = Cx<R>::make(fma(r, wy, fma(r2, c.x, -b.x)), fma(-r, wx, fma(r2, c.y, -b.y)));
-    }
-}
-
-#ifndef FQ_PAIR_RX
-#define FQ_PAIR_RX 1
-#endif
-
 // Butterflies of one coefficient set on the register bits in `mask`.
 // M: RX form 0 -> (1, t), 1 -> (u, 1), 3 -> chosen at run time.
-// RX: register bits (0, 1) and (2, 3) that are both targets run as one two-qubit
-// step (bfly_rx_pair); a lone target bit runs the single-qubit butterfly.
 template <int MIX, int M, int PAT, typename R>
 __device__ __forceinline__ void bfly16(C2<R> (&v)[kRegs], const CoefSet &C, int mask) {
     if (MIX == MIX_RX && M == 3) {
@@ -253,30 +192,6 @@ __device__ __forceinline__ void bfly16(C2<R> (&v)[kRegs], const CoefSet &C, int 
         else bfly16<MIX, 1, PAT, R>(v, C, mask);
         return;
     }
-    if constexpr (MIX == MIX_RX && FQ_PAIR_RX) {
-        const R r = (R)C.r, r2 = (R)(C.r * C.r);
-#pragma unroll
-        for (int j = 0; j < 4; j += 2) {
-            const bool b0 = (mask >> j) & 1, b1 = (mask >> (j + 1)) & 1;
-            if (b0 && b1) {
-#pragma unroll
-                for (int i = 0; i < kRegs; ++i)
-                    if (!(i & (3 << j)))
-                        bfly_rx_pair<M>(v[i], v[i | (1 << j)], v[i | (2 << j)], v[i | (3 << j)], r, r2);
-                continue;
-            }
-#pragma unroll
-            for (int jj = j; jj < j + 2; ++jj) {
-                if (!((mask >> jj) & 1)) continue;
-#pragma unroll
-                for (int i = 0; i < kRegs; ++i)
-                    if (!(i & (1 << jj))) {
-                        if (M == 0) bfly_rx0(v[i], v[i | (1 << jj)], r);
-                        else bfly_rx1(v[i], v[i | (1 << jj)], r);
-                    }
-            }
-        }
-    } else {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         if (!((mask >> j) & 1)) continue;
@@ -298,7 +213,6 @@ __device__ __forceinline__ void bfly16(C2<R> (&v)[kRegs], const CoefSet &C, int 
             for (int i = 0; i < kRegs; ++i)
                 if (!(i & (1 << j))) bfly_su2(v[i], v[i | (1 << j)], a, b);
         }
-    }
     }
 }
 
@@ -468,8 +382,7 @@ __device__ __forceinline__ int round_mask(const unsigned char *rt, int r) {
 //   K: target-mask class of the rounds (see round_mask): compile-time masks keep
 //       the butterfly code branch-free (run-time masks force register moves at
 //       every merge point).
-template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R = double, bool G = false,
-          bool CA = false>
+template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R = double, bool G = false>
 __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ PassParams P,
                                                         const __grid_constant__ CUtensorMap tm_state,
                                                         const __grid_constant__ CUtensorMap tm_cost) {
@@ -487,32 +400,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
     static_assert(!HEAVY || PH != 3, "PH = 3 (expectation preload) is a light-pass mode");
     constexpr int NR = seq_rounds(SEQ);
     constexpr int LAST = seq_pat(SEQ, NR - 1);
-    static_assert(!CA || (COST == FQ_COST_U16 && (PH == 1 || PH == 2) && !G), "CA: uint16 phase passes of one state");
-    // CA: two cost-slice buffers behind the phase tables
-    unsigned short *cbuf = reinterpret_cast<unsigned short *>(thi + (CA ? P.table_hi * table_copies<R>() : 0));
 
     if (COST == FQ_COST_U16 && (PH == 1 || PH == 2)) {
         if (P.table_hi > 0) build_phase_tables<R>(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
         __syncthreads();
     }
     constexpr int CB = COST == FQ_COST_F64 ? 8 : 2;
-    // CA: copy the cost slice of the tile at `b` into buffer `buf` (cp.async chunks of
-    // 2^cost_chunk_log2 contiguous elements; 0 -> plain loads + shared stores)
-    auto stage_costs = [&](long long b, int buf) {
-        unsigned short *dst = cbuf + buf * kCostPadded;
-        const unsigned short *src = static_cast<const unsigned short *>(P.costs) + b;
-        const int cl = P.cost_chunk_log2;
-        const int per = (kTile >> cl) / kThreads;  // chunks per thread
-        for (int j = 0; j < per; ++j) {
-            const int e = (tid + j * kThreads) << cl;
-            long long off = 0;
-#pragma unroll
-            for (int bit = 0; bit < kTileBits; ++bit)
-                if ((e >> bit) & 1) off += 1LL << P.tile_pos[bit];
-            if (cl > 0) cp_async_bytes(dst + cost_slot(e), src + off, 2 << cl);
-            else dst[cost_slot(e)] = __ldcs(src + off);
-        }
-    };
     const long long thr8 = thread_offset<PAT8, G>(P, tid);
     const long long thr4 = thread_offset<PAT4, G>(P, tid);
     const long long thrL = LAST == PAT8 ? thr8 : thr4;
@@ -539,19 +432,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
     // reverse passes walk the tiles from the top: the previous pass ended there,
     // so the first tiles read are still in L2 (written moments ago)
     long long base = tile_base(P, P.tile0 + (P.reverse ? P.n_tiles - 1 - blockIdx.x : blockIdx.x));
-    if constexpr (CA) {  // prologue: this CTA's first cost slice
-        if (blockIdx.x < P.n_tiles) stage_costs(base, 0);
-        cp_async_commit();
-    }
-    int cur = 0;  // CA: buffer holding this tile's cost slice
-    for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x, cur ^= 1,
+    for (long long t = blockIdx.x; t < P.n_tiles; t += gridDim.x,
                    base = P.reverse ? prev_base(base, P.tile_mask, P.step_dep) : next_base(base, P.tile_mask, P.step_dep)) {
-        if constexpr (CA) {  // the next tile's cost slice streams in while this tile is processed
-            if (t + gridDim.x < P.n_tiles)
-                stage_costs(P.reverse ? prev_base(base, P.tile_mask, P.step_dep) : next_base(base, P.tile_mask, P.step_dep),
-                            cur ^ 1);
-            cp_async_commit();
-        }
         if (pf) {
             const long long tp = t + (long long)P.pf_dist * gridDim.x;
             if (tp < P.n_tiles) prefetch_tile(P, &tm_state, &tm_cost, P.reverse ? P.n_tiles - 1 - tp : tp, !P.init);
@@ -568,24 +450,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
 #pragma unroll
             for (int i = 0; i < kRegs; ++i) v[i] = ld_stream(reinterpret_cast<const T *>(ps8 + P.roff[PAT8][i]));
         }
-        if (PH == 1 && !CA) {
+        if (PH == 1) {
             const char *c8 = cs + thr8 * CB;
 #pragma unroll
             for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c8 + P.coff[PAT8][i]);
-        }
-        if (PH == 1 && CA) {  // this tile's slice has landed (the next one may still be in flight)
-            cp_async_wait<1>();
-            __syncthreads();
-            const unsigned short *cb = cbuf + cur * kCostPadded;
-#pragma unroll
-            for (int i = 0; i < kRegs; ++i) raw[i] = cb[cost_slot(pat_elem<PAT8>(tid, i))];
         }
         if (PH == 3) {  // the program's last pass: its expectation costs, in the store pattern
             const char *cl = cs + thrL * CB + (LAST == PAT8 ? 0 : g4c());
 #pragma unroll
             for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i]);
         }
-        if (PH == 2 && !CA) {
+        if (PH == 2) {
             if (P.probe & 1) {
 #pragma unroll
                 for (int i = 0; i < kRegs; ++i) raw[i] = (CostRaw<COST>)((tid * 7 + i * 131) & 1023);
@@ -625,16 +500,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
             bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
             if (HAS_B) bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
         } else if constexpr (SEQ == SEQ_84048) {
-            if constexpr (CA) cp_async_wait<1>();
             transpose<PAT8, PAT0>(tile, v, tid);
             bfly16<MIX, MA, PAT0, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
             transpose<PAT0, PAT4>(tile, v, tid);
             bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 2));
-            if constexpr (CA) {
-                const unsigned short *cb = cbuf + cur * kCostPadded;
-#pragma unroll
-                for (int i = 0; i < kRegs; ++i) raw[i] = cb[cost_slot(pat_elem<PAT4>(tid, i))];
-            }
             phase_all();
             bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
             transpose<PAT4, PAT0>(tile, v, tid);
@@ -642,14 +511,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
             transpose<PAT0, PAT8>(tile, v, tid);
             bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 4));
         } else {  // SEQ_848
-            if constexpr (CA) cp_async_wait<1>();  // this tile's slice: published by the transpose's barrier
             transpose<PAT8, PAT4>(tile, v, tid);
             bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
-            if constexpr (CA) {
-                const unsigned short *cb = cbuf + cur * kCostPadded;
-#pragma unroll
-                for (int i = 0; i < kRegs; ++i) raw[i] = cb[cost_slot(pat_elem<PAT4>(tid, i))];
-            }
             phase_all();
             bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
             transpose<PAT4, PAT8>(tile, v, tid);
@@ -671,7 +534,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
             st_stream(reinterpret_cast<T *>(psl + P.roff[LAST][i]), x);
         }
     }
-    if constexpr (CA) cp_async_wait<0>();
     if (P.expect) {
         const double s = block_sum<kThreads>(eacc, red);
         if (tid == 0) P.partials[blockIdx.x] = s;
@@ -695,43 +557,20 @@ struct PassMaps {
     alignas(64) CUtensorMap cost;
 };
 
-// CA passes: uint16 phase passes of one state with compile-time masks (the
-// host sets P.cost_async when the two cost buffers fit beside two CTAs per SM)
-template <int MIX, int COST, int PH, int K, bool G>
-constexpr bool ca_eligible() {
-    return COST == FQ_COST_U16 && (PH == 1 || PH == 2) && !G && K != 0 && MIX == MIX_RX;
-}
-
-template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R, bool G, bool CA>
-static int launch_pass16_ca(const PassParams &P, const PassMaps &M, int grid, cudaStream_t st) {
-    static bool configured = false;
-    constexpr int CP = table_copies<R>();
-    constexpr size_t cbytes = CA ? 2 * kCostPadded * sizeof(unsigned short) : 0;
-    const size_t smem = (size_t)(kTilePadded + (kTableLo + kMaxTableHi) * CP) * sizeof(C2<R>) + cbytes;
-    if (!configured) {
-        cudaFuncSetAttribute(k_pass16<MIX, COST, SEQ, PH, MA, MB, K, R, G, CA>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
-    const size_t need = (size_t)(kTilePadded + (kTableLo + P.table_hi) * CP) * sizeof(C2<R>) + cbytes;
-    k_pass16<MIX, COST, SEQ, PH, MA, MB, K, R, G, CA><<<grid, kThreads, need, st>>>(P, M.state, M.cost);
-    FQ_LAUNCHED("k_pass16");
-    return FQ_OK;
-}
-
 template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R = double, bool G = false>
 static int launch_pass16(const PassParams &P, const PassMaps &M, int grid, cudaStream_t st) {
-    if constexpr (ca_eligible<MIX, COST, PH, K, G>()) {
-        if (P.cost_async) return launch_pass16_ca<MIX, COST, SEQ, PH, MA, MB, K, R, G, true>(P, M, grid, st);
+    static bool configured = false;
+    constexpr int CP = table_copies<R>();
+    const size_t smem = (size_t)(kTilePadded + (kTableLo + kMaxTableHi) * CP) * sizeof(C2<R>);
+    if (!configured) {
+        cudaFuncSetAttribute(k_pass16<MIX, COST, SEQ, PH, MA, MB, K, R, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        configured = true;
     }
-    return launch_pass16_ca<MIX, COST, SEQ, PH, MA, MB, K, R, G, false>(P, M, grid, st);
-}
-
-// Dynamic shared memory of a pass with the cost buffers (host check: two CTAs per SM)
-inline size_t pass_smem_bytes(bool c64, int table_hi, bool ca) {
-    const size_t el = c64 ? sizeof(float2) : sizeof(double2);
-    const int CP = (int)(128 / el);
-    return (kTilePadded + (size_t)(kTableLo + table_hi) * CP) * el + (ca ? 2 * kCostPadded * sizeof(unsigned short) : 0);
+    const size_t need = (size_t)(kTilePadded + (kTableLo + P.table_hi) * CP) * sizeof(C2<R>);
+    k_pass16<MIX, COST, SEQ, PH, MA, MB, K, R, G><<<grid, kThreads, need, st>>>(P, M.state, M.cost);
+    FQ_LAUNCHED("k_pass16");
+    return FQ_OK;
 }
 
 // Template dispatch for one round program SEQ of one (mixer, cost) pair.

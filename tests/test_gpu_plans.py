@@ -113,7 +113,10 @@ def _fingerprint(shards, idx, n_blocks=1024):
     K = len(shards)
     per = n_blocks // K
     size = shards[0].numel()
-    blocks = np.concatenate([(s.abs() ** 2).reshape(per, -1).sum(dim=1).double().cpu().numpy() for s in shards])
+    blk = size // per
+    # block by block: no full-size temporaries next to a 32-64 GiB state
+    blocks = torch.stack([torch.view_as_real(s[r * blk:(r + 1) * blk]).double().pow(2).sum()
+                          for s in shards for r in range(per)]).cpu().numpy()
     amp = np.empty(idx.size, dtype=np.complex128)
     for r, s in enumerate(shards):
         sel = (idx // size) == r
