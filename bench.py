@@ -43,6 +43,13 @@ sys.path.insert(0, ROOT)
 
 BASE_N = 26
 PASS_NAMES = {-1: "phase sweep", 0: "8|0|4", 1: "8|4", 2: "8|0|4|0|8", 3: "8|4|8"}
+
+
+def pass_name(sq: int) -> str:
+    """Round program of a pass record; >= 100: an L2 slab sweep of two passes."""
+    if sq >= 100:
+        return f"sweep[{PASS_NAMES[(sq - 100) // 10]} > {PASS_NAMES[(sq - 100) % 10]}]"
+    return PASS_NAMES.get(sq, str(sq))
 METRIC = "QAOA objective evals/sec (LABS/MaxCut n=26–34); achieved HBM GB/s vs peak"
 
 
@@ -177,6 +184,131 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------- extra BASELINE configs
+def _event_ms(fn, reps, world):
+    """Device time of `reps` calls, CUDA events on the current stream, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def run_config3(args):
+    """BASELINE config 3: LABS n=30 p=10 objective inside a COBYLA loop (scipy),
+    precompute once; evals/s including every evaluation's host round trip
+    (the optimiser's own time included), next to the reference algorithm's CPU
+    time at the same size (oracle port, 1 layer + expectation, extrapolated)."""
+    import torch
+    from scipy.optimize import minimize
+
+    from paper_2309_04841_b200 import QaoaSimulator, labs_terms
+
+    try:
+        n, p = 30, 10
+        t0 = time.perf_counter()
+        sim = QaoaSimulator(terms=labs_terms(n))
+        torch.cuda.synchronize()
+        pre = time.perf_counter() - t0
+        x0 = np.concatenate(angles(p)) * 0.1
+        calls = [0]
+
+        def f(x):
+            calls[0] += 1
+            return sim.objective(x[:p], x[p:])
+
+        f(x0)
+        torch.cuda.synchronize()
+        calls[0] = 0
+        t0 = time.perf_counter()
+        res = minimize(f, x0, method="COBYLA", options={"maxiter": args.cobyla_iters, "rhobeg": 0.05})
+        dt = time.perf_counter() - t0
+        ms_dev = _event_ms(lambda: sim.objective(res.x[:p], res.x[p:]), 2, 1)
+        out = {"workload": "LABS n=30 p=10 X-mixer complex128 objective inside scipy COBYLA "
+                           f"(maxiter {args.cobyla_iters}, rhobeg 0.05, x0 = 0.1 * default_rng(0) U(0,1))",
+               "evals": calls[0], "wall_s": dt, "evals_per_s": calls[0] / dt, "ms_per_eval_device": ms_dev,
+               "precompute_s": pre, "objective_start": float(f(x0)), "objective_end": float(res.fun),
+               "cost_encoding": "uint16" if sim.device_costs.u16 is not None else "float64"}
+        del sim
+        torch.cuda.empty_cache()
+        return out
+    except Exception as exc:  # noqa: BLE001 - an extra key never fails the headline line
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
+
+def run_config5(args, world, rank, k, barrier):
+    """BASELINE config 5 / north star: LABS n=34 p=10 complex128 sharded over the
+    N ranks (fused sharded program: local passes on each shard, global-group
+    passes spanning all shards over NVLink).  Per-layer ms and HBM roofline per
+    GPU (algorithmic bytes of the rank's passes / time).  One GPU cannot hold
+    the complex128 state (256 GiB): N = 1 reports complex64 n=34 (128 GiB), the
+    same problem at the optional precision.  The reference refuses n > 30
+    (terms.py:23), so there is no CPU point at this size."""
+    import torch
+
+    from paper_2309_04841_b200 import QaoaSimulator, _lib, labs_terms
+    from paper_2309_04841_b200.distributed import ShardedQaoaSimulator
+
+    n, p = 34, 10
+    g, b = angles(p)
+    try:
+        free, _ = torch.cuda.mem_get_info()
+        c64 = world == 1
+        elem = 8 if c64 else 16
+        n_local = n - k
+        if (1 << n_local) * (elem + 2) > 0.92 * free:
+            return {"skipped": f"n=34 needs {(1 << n_local) * (elem + 2) / 2**30:.0f} GiB per GPU, "
+                               f"{free / 2**30:.0f} GiB free"}
+        t0 = time.perf_counter()
+        if world == 1:
+            sim = QaoaSimulator(terms=labs_terms(n), dtype="complex64")
+            fn = lambda: sim.objective(g, b)  # noqa: E731
+        else:
+            sim = ShardedQaoaSimulator(labs_terms(n), global_mode="fused")
+            fn = lambda: sim.simulate_qaoa(g, b)  # noqa: E731
+        barrier()
+        pre = time.perf_counter() - t0
+        obj = float(fn())
+        ms = _event_ms(fn, 1, world)
+        S = elem * (1 << n_local)
+        lay = (_lib.FqLayer * p)(*[_lib.FqLayer(float(gi), float(bi), 1, 0, n) for gi, bi in zip(g, b)])
+        gp = ctypes.c_int()
+        if world == 1:
+            passes = _lib.load().fq_plan_x_passes(n, p, lay, _lib.STATE_C64)
+            gpv = 0
+        else:
+            passes = _lib.load().fq_plan_sharded_passes(n_local, k, p, lay, ctypes.byref(gp))
+            gpv = gp.value
+        C = 2 * (1 << n_local)
+        hbm = passes * 2 * S - S + (p + 1) * C
+        peak, _ = load_peaks()
+        out = {"workload": f"LABS n=34 p=10 X-mixer {'complex64 (complex128 needs 256 GiB)' if c64 else 'complex128'}"
+                           f" on {world} GPU(s), n_local={n_local}",
+               "ms_per_eval": ms, "ms_per_layer": ms / p, "precompute_s": pre, "objective": obj,
+               "passes_per_eval": passes, "spanning_passes_per_eval": gpv,
+               "hbm_bytes_per_gpu": hbm, "nvlink_bytes_per_gpu": gpv * 2 * S * (world - 1) // world,
+               "roofline_frac_hbm": hbm / (ms / 1e3) / 1e9 / peak,
+               "cpu_reference": "n/a: the reference refuses n > 30 (terms.py:23, MemoryError)"}
+        del sim
+        torch.cuda.empty_cache()
+        return out
+    except Exception as exc:  # noqa: BLE001 - an extra key never fails the headline line
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
+
 # ---------------------------------------------------------------------------- GPU
 def main():
     ap = argparse.ArgumentParser()
@@ -190,6 +322,9 @@ def main():
     ap.add_argument("--global-mode", default="fused", choices=["fused", "p2p", "exchange"],
                     help="N>1: one sharded program whose global-qubit passes span all shards over peer memory "
                          "(fused), a per-layer peer-memory global kernel (p2p), or NCCL all-to-all exchanges")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the extra BASELINE config keys (config3: COBYLA loop at n=30; config5: LABS n=34)")
+    ap.add_argument("--cobyla-iters", type=int, default=24)
     ap.add_argument("--state", default="c128", choices=["c128", "c64"],
                     help="state type: complex128 (the headline, the reference's) or the optional complex64")
     args = ap.parse_args()
@@ -216,6 +351,10 @@ def main():
         if one_device:
             dist.init_process_group("gloo")
         else:
+            # NCCL's communicator lines (nRanks, NVLink / NVLS transports) on stderr: the
+            # evidence that N ranks really formed one communicator over this node's GPUs
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2309_04841_b200 import QaoaSimulator, _lib, labs_terms
     from paper_2309_04841_b200.distributed import ShardedQaoaSimulator
@@ -281,9 +420,9 @@ def main():
             run_program(state, n, "x", layers, dc=dc, init=True, init_amp=amp, expectation_out=exp_dev)
     else:
         def step():
-            sim.simulate_qaoa(g, b, expectation=False)
-            loc = sim.ops.expectation(sim.shard, sim.costs)
-            dist.all_reduce(loc)
+            # the public call: one sharded program whose last pass accumulates this rank's
+            # objective partials, then one all-reduce (objective + barrier error word)
+            sim.simulate_qaoa(g, b)
 
     for _ in range(args.warmup):
         step()
@@ -302,7 +441,10 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    units_per_eval = 2.0 ** (n - BASE_N) if world > 1 else 1.0
+    # unit of work: weak scaling (default, n = 26 + log2 N) counts n=26-equivalent evaluations,
+    # so ideal scaling is N x the 1-GPU value; a fixed --qubits problem counts evaluations of it
+    # at every N (strong scaling) — the same unit at every world size
+    units_per_eval = 1.0 if args.n else 2.0 ** (n - BASE_N)
     value = args.steps * units_per_eval / (ms / 1e3)
 
     # ------------------------------------------------------------ byte model of the step (per GPU)
@@ -313,15 +455,21 @@ def main():
     P_survey = -(-n_local // 12)
     survey_bytes = p * (P_survey * 2 * S + Cb) + (S + Cb)
     if world == 1:
-        tile_bytes = passes * 2 * S - S + (n_phase + 1) * Cb  # first pass generates |+>, last reads costs for E
-        launches = passes + 1
+        # HBM round trips of the state actually run: the planned passes, minus one per
+        # L2 slab sweep (a sweep runs two passes over each L2-resident slab)
+        step()
+        torch.cuda.synchronize()
+        round_trips = _lib.load().fq_last_passes(None, None, 0)
+        sweeps = passes - round_trips
+        tile_bytes = round_trips * 2 * S - S + (n_phase + 1) * Cb  # first pass generates |+>, last reads costs for E
+        launches = round_trips + 1 + sweeps  # + the partials' sum, + one counter memset per sweep
     elif args.global_mode == "fused":
         # one sharded plan over all n qubits; its global-group passes span the shards
         glay = (_lib.FqLayer * p)(*[_lib.FqLayer(float(gi), float(bi), 1, 0, n) for gi, bi in zip(g, b)])
         gp = ctypes.c_int()
         passes = _lib.load().fq_plan_sharded_passes(n_local, k, p, glay, ctypes.byref(gp))
-        tile_bytes = passes * 2 * S - S + (n_phase + 1) * Cb
-        launches = passes + 2 * gp.value + 2  # + two device barriers per spanning pass, + the expectation (2)
+        tile_bytes = passes * 2 * S - S + (n_phase + 1) * Cb  # the last pass reads the costs for E (fused)
+        launches = passes + 2 * gp.value + 1  # + two device barriers per spanning pass, + the partials' sum
         nvlink_bytes = gp.value * 2 * S * (world - 1) // world
     else:
         post = p * (1 if k > 0 else 0)  # the k-position pass after each exchange
@@ -347,7 +495,7 @@ def main():
             for i in range(cnt):
                 sq, ph, nt, ini, ex = info[5 * i:5 * i + 5]
                 nb = (0 if ini else S) + S + (Cb if (ph or ex) else 0)
-                kd = kinds.setdefault(PASS_NAMES.get(sq, str(sq)) + (" +phase" if ph in (1, 2) else "") +
+                kd = kinds.setdefault(pass_name(sq) + (" +phase" if ph in (1, 2) else "") +
                                       (" +init" if ini else "") + (" +expect" if ex else ""),
                                       {"launches": 0, "ms": 0.0, "bytes": 0})
                 kd["launches"] += 1
@@ -417,6 +565,22 @@ def main():
                "h2d_bytes_per_step": 2 * p * 8, "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / args.steps,
                "api": "ShardedQaoaSimulator.simulate_qaoa"}
 
+    # ------------------------------------------------------------ N > 1: fused vs NCCL exchange, same run
+    crosscheck = None
+    if world > 1:
+        objective_fused = float(sim.simulate_qaoa(g, b))
+        if args.global_mode == "fused" and not c64:
+            try:
+                xsim = ShardedQaoaSimulator(poly, global_mode="exchange")
+                obj_x = float(xsim.simulate_qaoa(g, b))
+                crosscheck = {"fused_objective": objective_fused, "nccl_exchange_objective": obj_x,
+                              "rel_diff": abs(objective_fused - obj_x) / max(1e-300, abs(obj_x)),
+                              "exchanges_per_eval": xsim.exchange_count}
+                del xsim
+            except Exception as exc:  # noqa: BLE001 - reported in the line
+                crosscheck = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+            torch.cuda.empty_cache()
+
     # ------------------------------------------------------------ CPU baseline (rank 0, N = 1 only)
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu:
@@ -432,6 +596,15 @@ def main():
 
     if world > 1:
         objective = float(sim.expectation())  # collective
+
+    # ------------------------------------------------------------ BASELINE configs 3 and 5 (extra keys)
+    extra = {}
+    if not args.no_configs:
+        del sim, dc
+        torch.cuda.empty_cache()
+        if world == 1:
+            extra["config3"] = run_config3(args)
+        extra["config5"] = run_config5(args, world, rank, k, barrier)
     if rank == 0:
         line = {
             **({"validation_only": "all ranks on one GPU (FQ_BENCH_ONE_DEVICE)"} if one_device else {}),
@@ -463,6 +636,10 @@ def main():
                                              "C = cost bytes per amplitude * 2^n",
                          "achieved_whole_step": achieved_step,
                          "algorithmic_bytes_per_step": tile_bytes, "passes_per_step": passes if world == 1 else None,
+                         **({"hbm_round_trips_per_step": round_trips, "l2_sweeps_per_step": sweeps,
+                             "l2_note": "a sweep runs two passes per L2-resident slab: its second pass reads and "
+                                        "writes L2, not HBM (algorithmic HBM bytes count one round trip)"}
+                            if world == 1 else {}),
                          "by_pass_kind": kinds or None,
                          "survey_model": {"bytes_per_eval": survey_bytes, "evals_per_s_at_peak": peak * 1e9 / survey_bytes,
                                           "note": "SURVEY.md §8(d): P=ceil(n/12) unfused passes per layer"}},
@@ -470,6 +647,8 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches * args.steps,
             "clocks": sampler.summary(),
+            **({"crosscheck": crosscheck} if crosscheck else {}),
+            **extra,
             "precompute_s": precompute_s,
             "ms_per_layer": ms_step / p,
             "objective": objective,

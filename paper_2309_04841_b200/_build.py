@@ -19,7 +19,7 @@ LIB = os.path.join(HERE, "libfqaoa.so")
 SOURCES = ["ops.cu", "evolve.cu", "pass_rx_u16_light.cu", "pass_rx_u16_heavy.cu", "pass_rx_f64_light.cu",
            "pass_rx_f64_heavy.cu", "pass_su2.cu", "pass_su2_c64.cu", "pass_c64_u16.cu", "pass_c64_f64.cu", "pass_global_u16.cu",
            "pass_global_f64.cu", "pass_global_c64.cu", "xy.cu", "global.cu",
-           "wht.cu"]
+           "wht.cu", "sweep.cu", "sweep_c128_k3.cu", "sweep_c128_k4.cu", "sweep_c64_k3.cu", "sweep_c64_k4.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -37,6 +37,7 @@
 //    which is also the batched multi-parameter path for optimiser loops.
 #include <string>
 
+#include "sweep.cuh"
 #include "tmap.cuh"
 
 namespace fq {
@@ -289,6 +290,23 @@ static int g_prefetch = -1;  // L2 prefetch distance (grid strides); -1: 1 for r
 static int g_phase_tables = 1;
 static int g_plan = -1;      // -1: choose by cost model, else force style (0 / 1, legacy chunk sizes)
 static int g_plan_tmax = 0;  // > 0: force the high-group chunk size (4..12) of the X plan (parity tests of every shape)
+static int g_sweep = 1;          // run eligible pass pairs as L2-resident slab sweeps (sweep.cuh)
+static int g_sweep_team = 32;    // CTAs per sweep team
+static int g_sweep_slab_log2 = 23;  // largest slab (bytes, log2): 8 MiB x ~9 teams in flight stay in L2
+static long long g_sweeps_launched = 0;
+// scratch layout of the sweeps: team counters (16 x 128 B) and the barrier error word
+constexpr int kSweepCtrOffset = 2048;  // doubles
+constexpr int kSweepErrOffset = 2048 + 16 * 16;
+static int *S_err_ptr(const fq_evolve_desc *d) { return reinterpret_cast<int *>(d->scratch + kSweepErrOffset); }
+
+// sum of partials, NaN when a sweep's team barrier timed out (never a silent wrong objective)
+__global__ void k_sum_partials_checked(const double *partials, int count, const int *err, double *out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < count; ++i) t += partials[i];
+        *out = (*err) ? __longlong_as_double(0x7ff8000000000000LL) : t;
+    }
+}
 static int g_time_passes = 0;
 static int g_probe = 0;      // development probe bits (PassParams::probe)
 static int g_zigzag = 1;     // alternate the tile walk direction pass to pass (L2 reuse across passes)
@@ -633,35 +651,13 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCt
         return FQ_OK;
     };
     if (int s0 = mark(0)) return s0;
-    for (size_t si = 0; si < seq.size(); ++si) {
-        const PlannedPass &pp = seq[si];
-        const bool last = (si + 1 == seq.size());
-        if (pp.group < 0) {  // standalone phase, shard-local
-            g_last_plan.push_back({-1, 1, 0, init_pending ? 1 : 0, (last && d->expectation_dev) ? 1 : 0});
-            if (init_pending) {
-                if (int s = init_shards()) return s;
-                init_pending = false;
-            }
-            const fq_layer &L = d->layers[pp.phase_layer];
-            for (int r : mine) {
-                fq_evolve_desc e = shard_desc(r);
-                if (c64) launch_phase(static_cast<float2 *>(e.psi), &e, size, L.gamma, st);
-                else launch_phase(static_cast<double2 *>(e.psi), &e, size, L.gamma, st);
-                FQ_LAUNCHED("k_phase");
-            }
-            if (last && d->expectation_dev)
-                if (int s = expect_shards()) return s;
-            if (int s = mark(si + 1)) return s;
-            continue;
-        }
+    // PassParams of pass si_ of the plan (everything but the per-launch buffer /
+    // tile-range fields), its round program, phase mode and RX forms
+    auto build = [&](size_t si_, bool init_, bool expect_, PassParams &P, int &sq, int &ph, int &ma, int &mb,
+                     bool &two) {
+        const PlannedPass &pp = seq[si_];
         const Group &g = groups[pp.group];
-        const int gq = global_count(g, nv, kq);
-        if (gq != 0 && gq != kq) {
-            set_error("fq_qaoa_evolve_sharded: a group holds %d of the %d global qubits", gq, kq);
-            return FQ_ERR_UNSUPPORTED;
-        }
-        const bool global = gq > 0;
-        PassParams P;
+        const bool global = global_count(g, nv, kq) > 0;
         std::memset(&P, 0, sizeof P);
         P.cost_scale = d->cost_scale;
         P.cost_offset = d->cost_offset;
@@ -693,15 +689,14 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCt
                 P.coff[pat][i] = o * CB + (global ? P.cdelta[shard] : 0);
             }
         }
-        P.init = init_pending ? 1 : 0;
-        init_pending = false;
-        P.expect = (last && d->expectation_dev) ? 1 : 0;
+        P.init = init_ ? 1 : 0;
+        P.expect = expect_ ? 1 : 0;
         const int tmask = target_mask(g);
-        const bool two = pp.layerB >= 0;
-        const int sq = pass_seq(g, pp);
+        two = pp.layerB >= 0;
+        sq = pass_seq(g, pp);
         for (int r = 0; r < seq_rounds(sq); ++r)
             P.maskA[r] = P.maskB[r] = (unsigned char)((tmask >> pat_first_bit(seq_pat(sq, r))) & 15);
-        int ph = 0;
+        ph = 0;
         if (pp.phase_layer >= 0) {
             P.gamma = d->layers[pp.phase_layer].gamma;
             ph = pp.phase_at == 1 ? 1 : 2;
@@ -729,13 +724,147 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCt
         for (int i = 0; i < kTileBits; ++i)
             if (g.tile_pos[i] < nl) P.tile_mask |= 1LL << g.tile_pos[i];
         P.step_dep = deposit(grid, P.tile_mask);
-        P.reverse = g_zigzag ? (int)(si & 1) : 0;
+        P.reverse = g_zigzag ? (int)(si_ & 1) : 0;
         P.probe = g_probe;
         P.run_bits = 0;
         while (P.run_bits < kTileBits && g.tile_pos[P.run_bits] == P.run_bits) ++P.run_bits;
         P.pf_cost = (ph != 0 || P.expect) ? 1 : 0;
-        const int ma = P.A.mode, mb = two ? P.B.mode : 2;
+        ma = P.A.mode;
+        mb = two ? P.B.mode : 2;
         if (P.expect && ph == 0 && !two && !seq_heavy(sq)) ph = 3;  // preload the expectation's costs
+    };
+    // Passes si and si+1 as one L2-resident slab sweep (sweep.cuh) when the
+    // pair has an instantiation and its slab fits the L2 budget; `swept` tells.
+    bool sweep_err_reset = false;
+    auto sweep_pair = [&](size_t si, bool /*last*/, bool &swept) -> int {
+        swept = false;
+        const bool last2 = si + 2 == seq.size();
+        const Group &g1 = groups[seq[si].group], &g2 = groups[seq[si + 1].group];
+        if (global_count(g1, nv, kq) || global_count(g2, nv, kq)) return FQ_OK;
+        long long U = 0;  // slab bits
+        for (int i = 0; i < kTileBits; ++i) U |= (1LL << g1.tile_pos[i]) | (1LL << g2.tile_pos[i]);
+        const int ub = __builtin_popcountll(U);
+        const int log2_tiles = ub - kTileBits;
+        const int team = std::max(1, g_sweep_team);
+        if ((1 << log2_tiles) < team || (elem << ub) > (1LL << g_sweep_slab_log2)) return FQ_OK;
+        const long long n_slabs = 1LL << (nl - ub);
+        const int n_teams = (int)std::min<long long>({(long long)(2 * sms) / team, n_slabs, 16LL});
+        if (n_teams < 1) return FQ_OK;
+        PassParams P1, P2;
+        int sq1, ph1, ma1, mb1, sq2, ph2, ma2, mb2;
+        bool two1, two2;
+        build(si, init_pending, false, P1, sq1, ph1, ma1, mb1, two1);
+        build(si + 1, false, last2 && d->expectation_dev, P2, sq2, ph2, ma2, mb2, two2);
+        if ((ph1 == 1 || ph1 == 2) && (ph2 == 1 || ph2 == 2)) return FQ_OK;
+        SweepKind kind{sq1, ph1, ma1, mb1, mask_class(sq1, P1.maskA), sq2, ph2, ma2, mb2, mask_class(sq2, P2.maskA)};
+        if (!sweep_supported(mix, d->cost_kind, c64, kind)) return FQ_OK;
+        SweepParams *S = new SweepParams;
+        std::memset(S, 0, sizeof *S);
+        S->P1 = P1;
+        S->P2 = P2;
+        for (PassParams *Q : {&S->P1, &S->P2}) {
+            Q->psi = d->psi;
+            Q->costs = d->costs;
+            Q->partials = d->scratch;
+            Q->pf_dist = 0;
+        }
+        // tile-number bits of each sub-pass: slab-inner bits (U minus its tile bits), then the slab index
+        auto fill_dep = [&](const Group &g, unsigned char *dep) {
+            long long tb = 0;
+            for (int i = 0; i < kTileBits; ++i) tb |= 1LL << g.tile_pos[i];
+            int c = 0;
+            for (int b = 0; b < nl; ++b)
+                if (((U >> b) & 1) && !((tb >> b) & 1)) dep[c++] = (unsigned char)b;
+            for (int b = 0; b < nl; ++b)
+                if (!((U >> b) & 1)) dep[c++] = (unsigned char)b;
+        };
+        fill_dep(g1, S->dep1);
+        fill_dep(g2, S->dep2);
+        S->n_dep = nl - kTileBits;
+        S->log2_tiles = log2_tiles;
+        S->n_slabs = n_slabs;
+        S->team_size = team;
+        S->n_teams = n_teams;
+        // sub-pass 2's cost slice, per slab: runs of the slab's low contiguous bits (<= 2^14 levels)
+        const bool costs2 = ph2 != 0 || S->P2.expect;
+        int rb = 0;
+        while (rb < nl && ((U >> rb) & 1)) ++rb;
+        rb = std::min(rb, 14);
+        if (costs2 && d->cost_kind == FQ_COST_U16 && rb >= 3) {
+            S->cost_run_log2 = rb;
+            S->log2_cost_runs = ub - rb;
+            int c = 0;
+            for (int b = rb; b < nl; ++b)
+                if ((U >> b) & 1) S->cdep[c++] = (unsigned char)b;
+            for (int b = 0; b < nl; ++b)
+                if (!((U >> b) & 1)) S->cdep[c++] = (unsigned char)b;
+        }
+        S->pf1_bytes = (run_bits_of(g1) == kTileBits && !P1.init) ? (int)(elem << kTileBits) : 0;
+        unsigned *ctr = reinterpret_cast<unsigned *>(d->scratch + kSweepCtrOffset);
+        S->counters = ctr;
+        S->err = reinterpret_cast<int *>(d->scratch + kSweepErrOffset);
+        if (!sweep_err_reset) {
+            cudaError_t e = cudaMemsetAsync(S->err, 0, sizeof(int), st);
+            if (e != cudaSuccess) { delete S; return cuda_status(e, "cudaMemsetAsync(sweep err)"); }
+            sweep_err_reset = true;
+        }
+        cudaError_t e = cudaMemsetAsync(ctr, 0, 16 * 32 * sizeof(unsigned), st);
+        if (e != cudaSuccess) { delete S; return cuda_status(e, "cudaMemsetAsync(sweep counters)"); }
+        const int s = launch_sweep(mix, d->cost_kind, c64, kind, *S, st);
+        delete S;
+        if (s) return s;
+        init_pending = false;
+        swept = true;
+        g_last_plan.push_back({100 + 10 * sq1 + sq2, ph1 ? ph1 : ph2, (int)g2.targets.size(), P1.init, P2.expect});
+        if (P2.expect) {
+            k_sum_partials_checked<<<1, 32, 0, st>>>(d->scratch, n_teams * team, S_err_ptr(d), d->expectation_dev);
+            FQ_LAUNCHED("k_sum_partials_checked");
+        }
+        ++g_sweeps_launched;
+        return FQ_OK;
+    };
+    for (size_t si = 0; si < seq.size(); ++si) {
+        const PlannedPass &pp = seq[si];
+        const bool last = (si + 1 == seq.size());
+        if (pp.group < 0) {  // standalone phase, shard-local
+            g_last_plan.push_back({-1, 1, 0, init_pending ? 1 : 0, (last && d->expectation_dev) ? 1 : 0});
+            if (init_pending) {
+                if (int s = init_shards()) return s;
+                init_pending = false;
+            }
+            const fq_layer &L = d->layers[pp.phase_layer];
+            for (int r : mine) {
+                fq_evolve_desc e = shard_desc(r);
+                if (c64) launch_phase(static_cast<float2 *>(e.psi), &e, size, L.gamma, st);
+                else launch_phase(static_cast<double2 *>(e.psi), &e, size, L.gamma, st);
+                FQ_LAUNCHED("k_phase");
+            }
+            if (last && d->expectation_dev)
+                if (int s = expect_shards()) return s;
+            if (int s = mark(g_last_plan.size())) return s;
+            continue;
+        }
+        if (g_sweep && !sh && si + 1 < seq.size() && seq[si + 1].group >= 0) {
+            bool swept = false;
+            if (int s = sweep_pair(si, last, swept)) return s;
+            if (swept) {
+                ++si;  // the pair ran as one sweep
+                if (int s2 = mark(g_last_plan.size())) return s2;
+                continue;
+            }
+        }
+        const Group &g = groups[pp.group];
+        const int gq = global_count(g, nv, kq);
+        if (gq != 0 && gq != kq) {
+            set_error("fq_qaoa_evolve_sharded: a group holds %d of the %d global qubits", gq, kq);
+            return FQ_ERR_UNSUPPORTED;
+        }
+        const bool global = gq > 0;
+        PassParams P;
+        int sq, ph, ma, mb;
+        bool two;
+        build(si, init_pending, last && d->expectation_dev, P, sq, ph, ma, mb, two);
+        init_pending = false;
         int launches = 0;
         if (global) {
             // one pass over every shard: rank r takes its 1/K of the tiles (in-process: all)
@@ -800,7 +929,7 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCt
             k_sum_partials<<<1, 32, 0, st>>>(d->scratch, launches, d->expectation_dev);
             FQ_LAUNCHED("k_sum_partials");
         }
-        if (int s2 = mark(si + 1)) return s2;
+        if (int s2 = mark(g_last_plan.size())) return s2;
     }
     return FQ_OK;
 }
@@ -1041,6 +1170,9 @@ int fq_set_option(const char *name, int value) {
         {"phase_tables", &g_phase_tables, 0, 1},  // uint16 phase via smem tables (else sincos)
         {"plan", &g_plan, -1, 1},           // group plan: -1 cost model, 0 legacy, 1 small fusion groups
         {"plan_tmax", &g_plan_tmax, 0, 12},  // force the high-group chunk size (0: cost model)
+        {"sweep", &g_sweep, 0, 1},          // L2-resident slab sweeps of pass pairs
+        {"sweep_team", &g_sweep_team, 1, 256},  // CTAs per sweep team
+        {"sweep_slab_log2", &g_sweep_slab_log2, 16, 30},  // largest sweep slab, log2 bytes
         {"time_passes", &g_time_passes, 0, 1},  // CUDA events around every pass (fq_last_passes)
         {"xy_tiled", &g_xy_tiled, 0, 1},    // tiled XY passes (0: one kernel per gate)
         {"zigzag", &g_zigzag, 0, 1},        // alternate tile walk direction pass to pass

@@ -368,6 +368,158 @@ __device__ __forceinline__ int round_mask(const unsigned char *rt, int r) {
     else return seq_pat(SEQ, r) == PAT4 ? ((0xF << (4 - K)) & 0xF) : 0xF;
 }
 
+// Global-memory access modes of a tile: LD_STREAM / ST_STREAM evict-first
+// streaming (one HBM round trip per pass); LD_L2 reads through L2 only (data a
+// previous sub-pass of a slab sweep left there); ST_L2_KEEP stores with an
+// L2::evict_last policy (the next sub-pass re-reads it from L2).
+enum { LD_STREAM = 0, LD_L2 = 1 };
+enum { ST_STREAM = 0, ST_L2_KEEP = 1 };
+
+template <int LD, typename T>
+__device__ __forceinline__ T tile_load(const T *p) {
+    if constexpr (LD == LD_L2) return __ldcg(p);
+    else return ld_stream(p);
+}
+
+__device__ __forceinline__ void st_keep(double2 *p, double2 v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep(float2 *p, float2 v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
+}
+
+template <int ST, typename T>
+__device__ __forceinline__ void tile_store(T *p, T v, unsigned long long pol) {
+    if constexpr (ST == ST_L2_KEEP) st_keep(p, v, pol);
+    else st_stream(p, v);
+}
+
+__device__ __forceinline__ unsigned long long l2_evict_last_policy() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// One tile of a pass: load (or generate |+>), the round program SEQ with its
+// phase / expectation, store.  `base`: the tile's physical base index.
+// Shared by k_pass16 (one tile after another, streaming) and k_sweep (two
+// sub-passes per L2-resident slab).
+template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R, bool G, int LD, int ST>
+__device__ __forceinline__ void pass_tile(const PassParams &P, long long base, C2<R> *tile, const C2<R> *tlo,
+                                          const C2<R> *thi, long long thr8, long long thr4, double &eacc,
+                                          unsigned long long pol) {
+    using T = C2<R>;
+    const int tid = threadIdx.x;
+    constexpr bool HAS_B = MB != 2;
+    constexpr int NR = seq_rounds(SEQ);
+    constexpr int LAST = seq_pat(SEQ, NR - 1);
+    constexpr int CB = COST == FQ_COST_F64 ? 8 : 2;
+    const long long thrL = LAST == PAT8 ? thr8 : thr4;
+    auto g4s = [&]() -> long long {
+        if constexpr (G) return P.sdelta[(tid >> P.gshift) & P.gmask];
+        else return 0;
+    };
+    auto g4c = [&]() -> long long {
+        if constexpr (G) return P.cdelta[(tid >> P.gshift) & P.gmask];
+        else return 0;
+    };
+            // per-tile base pointers; the registers' offsets are constant-bank byte offsets
+            const char *ps8 = reinterpret_cast<const char *>(static_cast<T *>(P.psi) + base + thr8);
+            const char *cs = static_cast<const char *>(P.costs) + base * CB;
+            T v[kRegs];
+            CostRaw<COST> raw[kRegs];  // cost entries of the phase round, loaded with the state
+            if (P.init) {
+    #pragma unroll
+                for (int i = 0; i < kRegs; ++i) v[i] = Cx<R>::make((R)P.init_amp, (R)0);
+            } else {
+    #pragma unroll
+                for (int i = 0; i < kRegs; ++i) v[i] = tile_load<LD>(reinterpret_cast<const T *>(ps8 + P.roff[PAT8][i]));
+            }
+            if (PH == 1) {
+                const char *c8 = cs + thr8 * CB;
+    #pragma unroll
+                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c8 + P.coff[PAT8][i]);
+            }
+            if (PH == 3) {  // the program's last pass: its expectation costs, in the store pattern
+                const char *cl = cs + thrL * CB + (LAST == PAT8 ? 0 : g4c());
+    #pragma unroll
+                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i]);
+            }
+            if (PH == 2) {
+                if (P.probe & 1) {
+    #pragma unroll
+                    for (int i = 0; i < kRegs; ++i) raw[i] = (CostRaw<COST>)((tid * 7 + i * 131) & 1023);
+                } else {
+                    const char *c4 = cs + thr4 * CB + g4c();
+    #pragma unroll
+                    for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c4 + P.coff[PAT4][i]);
+                }
+            }
+            auto phase_all = [&]() {
+                // keep the table lookups behind the preceding butterflies: hoisted
+                // early they would hold 64 registers of phase factors and spill
+                asm volatile("" ::: "memory");
+                if (P.probe & 4) return;
+                if (P.probe & 2) {
+    #pragma unroll
+                    for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase16<COST, R>(P, (CostRaw<COST>)0, tlo, thi));
+                    return;
+                }
+    #pragma unroll
+                for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase16<COST, R>(P, raw[i], tlo, thi));
+            };
+            // ---- round 0 (PAT8)
+            if (PH == 1) phase_all();
+            bfly16<MIX, MA, PAT8, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 0));
+            if constexpr (SEQ == SEQ_840) {
+                if (HAS_B) bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 0));
+                transpose<PAT8, PAT0>(tile, v, tid);
+                bfly16<MIX, MA, PAT0, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+                if (HAS_B) bfly16<MIX, MB, PAT0, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
+                transpose<PAT0, PAT4>(tile, v, tid);
+                bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 2));
+                if (HAS_B) bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
+            } else if constexpr (SEQ == SEQ_84) {
+                if (HAS_B) bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 0));
+                transpose<PAT8, PAT4>(tile, v, tid);
+                bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+                if (HAS_B) bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
+            } else if constexpr (SEQ == SEQ_84048) {
+                transpose<PAT8, PAT0>(tile, v, tid);
+                bfly16<MIX, MA, PAT0, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+                transpose<PAT0, PAT4>(tile, v, tid);
+                bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 2));
+                phase_all();
+                bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
+                transpose<PAT4, PAT0>(tile, v, tid);
+                bfly16<MIX, MB, PAT0, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 3));
+                transpose<PAT0, PAT8>(tile, v, tid);
+                bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 4));
+            } else {  // SEQ_848
+                transpose<PAT8, PAT4>(tile, v, tid);
+                bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+                phase_all();
+                bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
+                transpose<PAT4, PAT8>(tile, v, tid);
+                bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
+            }
+            // ---- store (+ expectation) in the last round's pattern
+            const R fs = (R)P.final_scale;
+            if (PH != 3 && P.expect) {  // cost entries of the last pattern (final pass with a phase)
+                const char *cl = cs + thrL * CB + (LAST == PAT8 ? 0 : g4c());
+    #pragma unroll
+                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i]);
+            }
+            char *psl = reinterpret_cast<char *>(static_cast<T *>(P.psi) + base + thrL) + (LAST == PAT8 ? 0 : g4s());
+    #pragma unroll
+            for (int i = 0; i < kRegs; ++i) {
+                T x = v[i];
+                if (MIX == MIX_RX) x = Cx<R>::make(x.x * fs, x.y * fs);
+                if (P.expect) eacc += decode_cost<COST>(P, raw[i]) * ((double)x.x * x.x + (double)x.y * x.y);
+                tile_store<ST>(reinterpret_cast<T *>(psl + P.roff[LAST][i]), x, pol);
+            }
+}
+
 // ---------------------------------------------------------------- the pass kernel
 // Register-load pass, 256 threads x 16 amplitudes per 2^12 tile, 2 CTAs/SM
 // (grid-stride over tiles).  Everything that varies between passes of one
@@ -398,28 +550,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
     static_assert(!HEAVY || (PH == 2 && HAS_B), "heavy round programs carry the mid-layer phase");
     static_assert(HEAVY || PH != 2, "the mid-layer phase needs a heavy round program");
     static_assert(!HEAVY || PH != 3, "PH = 3 (expectation preload) is a light-pass mode");
-    constexpr int NR = seq_rounds(SEQ);
-    constexpr int LAST = seq_pat(SEQ, NR - 1);
 
     if (COST == FQ_COST_U16 && (PH == 1 || PH == 2)) {
         if (P.table_hi > 0) build_phase_tables<R>(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
         __syncthreads();
     }
-    constexpr int CB = COST == FQ_COST_F64 ? 8 : 2;
+    // G: PAT4's thread bits include the shard index (PAT8's never do); the
+    // shard byte offsets are re-read from the parameter bank at each use
     const long long thr8 = thread_offset<PAT8, G>(P, tid);
     const long long thr4 = thread_offset<PAT4, G>(P, tid);
-    const long long thrL = LAST == PAT8 ? thr8 : thr4;
-    // G: PAT4's thread bits include the shard index (PAT8's never do): this
-    // thread's shard byte offsets in the state / cost vector (0 otherwise),
-    // re-read from the parameter bank at each use (not held in registers)
-    auto g4s = [&]() -> long long {
-        if constexpr (G) return P.sdelta[(tid >> P.gshift) & P.gmask];
-        else return 0;
-    };
-    auto g4c = [&]() -> long long {
-        if constexpr (G) return P.cdelta[(tid >> P.gshift) & P.gmask];
-        else return 0;
-    };
     double eacc = 0.0;
 
     const bool pf = P.pf_dist > 0 && tid == 0;
@@ -438,101 +577,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
             const long long tp = t + (long long)P.pf_dist * gridDim.x;
             if (tp < P.n_tiles) prefetch_tile(P, &tm_state, &tm_cost, P.reverse ? P.n_tiles - 1 - tp : tp, !P.init);
         }
-        // per-tile base pointers; the registers' offsets are constant-bank byte offsets
-        const char *ps8 = reinterpret_cast<const char *>(static_cast<T *>(P.psi) + base + thr8);
-        const char *cs = static_cast<const char *>(P.costs) + base * CB;
-        T v[kRegs];
-        CostRaw<COST> raw[kRegs];  // cost entries of the phase round, loaded with the state
-        if (P.init) {
-#pragma unroll
-            for (int i = 0; i < kRegs; ++i) v[i] = Cx<R>::make((R)P.init_amp, (R)0);
-        } else {
-#pragma unroll
-            for (int i = 0; i < kRegs; ++i) v[i] = ld_stream(reinterpret_cast<const T *>(ps8 + P.roff[PAT8][i]));
-        }
-        if (PH == 1) {
-            const char *c8 = cs + thr8 * CB;
-#pragma unroll
-            for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c8 + P.coff[PAT8][i]);
-        }
-        if (PH == 3) {  // the program's last pass: its expectation costs, in the store pattern
-            const char *cl = cs + thrL * CB + (LAST == PAT8 ? 0 : g4c());
-#pragma unroll
-            for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i]);
-        }
-        if (PH == 2) {
-            if (P.probe & 1) {
-#pragma unroll
-                for (int i = 0; i < kRegs; ++i) raw[i] = (CostRaw<COST>)((tid * 7 + i * 131) & 1023);
-            } else {
-                const char *c4 = cs + thr4 * CB + g4c();
-#pragma unroll
-                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c4 + P.coff[PAT4][i]);
-            }
-        }
-        auto phase_all = [&]() {
-            // keep the table lookups behind the preceding butterflies: hoisted
-            // early they would hold 64 registers of phase factors and spill
-            asm volatile("" ::: "memory");
-            if (P.probe & 4) return;
-            if (P.probe & 2) {
-#pragma unroll
-                for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase16<COST, R>(P, (CostRaw<COST>)0, tlo, thi));
-                return;
-            }
-#pragma unroll
-            for (int i = 0; i < kRegs; ++i) v[i] = cmul(v[i], phase16<COST, R>(P, raw[i], tlo, thi));
-        };
-        // ---- round 0 (PAT8)
-        if (PH == 1) phase_all();
-        bfly16<MIX, MA, PAT8, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 0));
-        if constexpr (SEQ == SEQ_840) {
-            if (HAS_B) bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 0));
-            transpose<PAT8, PAT0>(tile, v, tid);
-            bfly16<MIX, MA, PAT0, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
-            if (HAS_B) bfly16<MIX, MB, PAT0, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
-            transpose<PAT0, PAT4>(tile, v, tid);
-            bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 2));
-            if (HAS_B) bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
-        } else if constexpr (SEQ == SEQ_84) {
-            if (HAS_B) bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 0));
-            transpose<PAT8, PAT4>(tile, v, tid);
-            bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
-            if (HAS_B) bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
-        } else if constexpr (SEQ == SEQ_84048) {
-            transpose<PAT8, PAT0>(tile, v, tid);
-            bfly16<MIX, MA, PAT0, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
-            transpose<PAT0, PAT4>(tile, v, tid);
-            bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 2));
-            phase_all();
-            bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
-            transpose<PAT4, PAT0>(tile, v, tid);
-            bfly16<MIX, MB, PAT0, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 3));
-            transpose<PAT0, PAT8>(tile, v, tid);
-            bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 4));
-        } else {  // SEQ_848
-            transpose<PAT8, PAT4>(tile, v, tid);
-            bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
-            phase_all();
-            bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
-            transpose<PAT4, PAT8>(tile, v, tid);
-            bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
-        }
-        // ---- store (+ expectation) in the last round's pattern
-        const R fs = (R)P.final_scale;
-        if (PH != 3 && P.expect) {  // cost entries of the last pattern (final pass with a phase)
-            const char *cl = cs + thrL * CB + (LAST == PAT8 ? 0 : g4c());
-#pragma unroll
-            for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i]);
-        }
-        char *psl = reinterpret_cast<char *>(static_cast<T *>(P.psi) + base + thrL) + (LAST == PAT8 ? 0 : g4s());
-#pragma unroll
-        for (int i = 0; i < kRegs; ++i) {
-            T x = v[i];
-            if (MIX == MIX_RX) x = Cx<R>::make(x.x * fs, x.y * fs);
-            if (P.expect) eacc += decode_cost<COST>(P, raw[i]) * ((double)x.x * x.x + (double)x.y * x.y);
-            st_stream(reinterpret_cast<T *>(psl + P.roff[LAST][i]), x);
-        }
+        pass_tile<MIX, COST, SEQ, PH, MA, MB, K, R, G, LD_STREAM, ST_STREAM>(P, base, tile, tlo, thi, thr8, thr4, eacc, 0ull);
     }
     if (P.expect) {
         const double s = block_sum<kThreads>(eacc, red);

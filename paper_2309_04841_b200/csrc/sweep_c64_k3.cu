@@ -1,0 +1,10 @@
+// k_sweep instantiations: float state, heavy mask class K2 = 3.
+#include "sweep_impl.cuh"
+
+namespace fq {
+
+int sweep_c64_k3(const SweepKind &k, const SweepParams &S, cudaStream_t st, bool dry) {
+    return sweep_dispatch<float, 3>(k, S, st, dry);
+}
+
+}  // namespace fq

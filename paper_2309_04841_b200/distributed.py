@@ -707,11 +707,20 @@ class ShardedQaoaSimulator:
         self.exchange_count += ex
         instrumentation.bump("exchange", ex)
         self._state = psi
-        self.check_barrier()  # mandatory after every peer-memory program
         if not expectation:
+            self.check_barrier()  # mandatory after every peer-memory program
             return None
-        dist.all_reduce(exp, op=dist.ReduceOp.SUM, group=self.group)
-        return float(exp.item())
+        # one host synchronisation: the objective's partial sums and every rank's
+        # barrier error word are all-reduced together
+        out = torch.stack([exp[0], self._flags[K].to(torch.float64)])
+        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=self.group)
+        e, err = out.tolist()
+        if err != 0.0:
+            self._flags[K].zero_()
+            self._broken = ("peer barrier timed out on some rank (a rank did not arrive); the sharded state is "
+                            "undefined — create a new ShardedQaoaSimulator")
+            raise RuntimeError(self._broken)
+        return e
 
     def close(self) -> None:
         for ptr, off in self._opened:

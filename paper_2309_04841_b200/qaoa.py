@@ -259,6 +259,14 @@ class QaoaSimulator:
             out = self._buffer
         return _evolve(self._dc, self.n, self.mixer, params, initial, out=out, dtype=self.dtype)
 
+    def objective(self, gammas: Sequence[float], betas: Sequence[float], initial=None) -> float:
+        """<C> of one parameter set — the optimiser-loop call (reference
+        qaoa_objective, qaoa.py:185-194, bound to this simulator): the
+        evolution runs in the simulator-owned state buffer and the objective
+        comes from the program's last pass; one host synchronisation."""
+        res = self.simulate_qaoa(gammas, betas, initial=initial, reuse_buffer=True)
+        return float(res.cached_expectation().item())
+
     def simulate_qaoa_batched(self, gammas, betas) -> np.ndarray:
         """Expectations of many parameter sets at once (n <= 12: each set
         runs in its own CTA, one launch).  gammas, betas: [batch, p]."""

@@ -47,6 +47,11 @@ def main():
             layers = [(float(x), float(y), 1, 0, n) for x, y in zip(gam, b)]
             lay = (_lib.FqLayer * p)(*[_lib.FqLayer(*t) for t in layers])
             passes = _lib.load().fq_plan_x_passes(n, p, lay, _lib.STATE_C64 if args.state == "c64" else 0)
+            if args.detail or True:  # HBM round trips actually run (sweeps fuse pass pairs)
+                fn0 = lambda: run_program(state, n, "x", layers, dc=dc, init=True, init_amp=1 / math.sqrt(1 << n),
+                                          expectation_out=e)
+                fn0()
+                passes = _lib.load().fq_last_passes(None, None, 0)
             fn = lambda: run_program(state, n, "x", layers, dc=dc, init=True, init_amp=1 / math.sqrt(1 << n),
                                      expectation_out=e)
             for _ in range(3):
@@ -72,6 +77,9 @@ def main():
                 cnt = _lib.load().fq_last_passes(info, tms, 64)
                 _lib.call("fq_set_option", b"time_passes", 0)
                 names_seq = {-1: "phase", 0: "8|0|4", 1: "8|4", 2: "8|0|4|0|8", 3: "8|4|8"}
+                for a in range(4):
+                    for c in range(4):
+                        names_seq[100 + 10 * a + c] = f"[{names_seq[a]}>{names_seq[c]}]"
                 for i in range(cnt):
                     sq, ph, nt, ini, ex = info[5 * i:5 * i + 5]
                     nb = (0 if ini else S) + S + (C if (ph or ex) else 0)

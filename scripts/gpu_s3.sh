@@ -1,0 +1,10 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+T=${1:-s3}
+timeout 600 python -m pytest tests/test_gpu_sweep.py -q -x > gpurun_out/pytest_sweep_$T.log 2>&1; echo "exit $?" >> gpurun_out/pytest_sweep_$T.log
+timeout 300 python scripts/bench_pass.py --opts "sweep=1,0" --detail > gpurun_out/pass_$T.log 2>&1
+timeout 300 python scripts/bench_pass.py --opts "sweep_team=16,32,37,64" > gpurun_out/pass_team_$T.log 2>&1
+timeout 300 python scripts/bench_pass.py --state c64 --opts "sweep=1,0" > gpurun_out/pass_c64_$T.log 2>&1
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_$T.log 2>&1
+echo done
