@@ -598,6 +598,7 @@ def main():
         objective = float(sim.expectation())  # collective
 
     # ------------------------------------------------------------ BASELINE configs 3 and 5 (extra keys)
+    cost_encoding = "uint16 levels (lossless)" if dc.u16 is not None else "float64"
     extra = {}
     if not args.no_configs:
         del sim, dc
@@ -616,7 +617,7 @@ def main():
                                    + (f" sharded over {world} GPUs (n_local={n_local}; value in n=26-equivalent "
                                       f"evaluations)" if world > 1 else ""),
                        "n": n, "p": p, "n_local": n_local, "angles": "default_rng(0) U(0,1)",
-                       "cost_encoding": "uint16 levels (lossless)" if dc.u16 is not None else "float64",
+                       "cost_encoding": cost_encoding,
                        "l2": (f"no flush: {S / 2**30:.2f} GiB state per GPU >> 126 MB L2" if S > (256 << 20)
                               else f"state of {S >> 20} MiB per GPU is L2-sized (validation sizes only)"),
                        "parallelism": (f"state sharded over {world} GPUs by global qubits, global-qubit mixer: "

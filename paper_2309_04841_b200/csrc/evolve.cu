@@ -290,7 +290,7 @@ static int g_prefetch = -1;  // L2 prefetch distance (grid strides); -1: 1 for r
 static int g_phase_tables = 1;
 static int g_plan = -1;      // -1: choose by cost model, else force style (0 / 1, legacy chunk sizes)
 static int g_plan_tmax = 0;  // > 0: force the high-group chunk size (4..12) of the X plan (parity tests of every shape)
-static int g_sweep = 1;          // run eligible pass pairs as L2-resident slab sweeps (sweep.cuh)
+static int g_sweep = 0;          // run eligible pass pairs as L2-resident slab sweeps (sweep.cuh); off: measured slower
 static int g_sweep_team = 32;    // CTAs per sweep team
 static int g_sweep_slab_log2 = 23;  // largest slab (bytes, log2): 8 MiB x ~9 teams in flight stay in L2
 static long long g_sweeps_launched = 0;
