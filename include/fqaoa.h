@@ -214,6 +214,13 @@ int fq_qaoa_evolve_batched(int n, int mixer, const void *costs, int cost_kind, d
                            double offset, int p, int batch, const double *gammas,
                            const double *betas, const void *psi_init, void *psi_out,
                            double *out_dev, void *stream);
+/* The same with the number of uint16 cost levels (cost_kind = FQ_COST_U16:
+ * the phase then comes from two e^{-i gamma c} tables per layer instead of a
+ * sincos per amplitude; 0 = unknown).  Parameter sets run one per CTA. */
+int fq_qaoa_evolve_batched_levels(int n, int mixer, const void *costs, int cost_kind, double scale,
+                                  double offset, int cost_levels, int p, int batch,
+                                  const double *gammas, const double *betas, const void *psi_init,
+                                  void *psi_out, double *out_dev, void *stream);
 
 /* A state sharded over K = 2^k ranks by its top k ("global") qubits
  * (reference distributed.py:51-54): shard r holds global indices

@@ -71,6 +71,7 @@ _SIGS = {
     "fq_qaoa_evolve_sharded": ([ctypes.POINTER(FqEvolveDesc), ctypes.POINTER(FqShardDesc), P], I),
     "fq_plan_sharded_passes": ([I, I, I, ctypes.POINTER(FqLayer), P], I),
     "fq_qaoa_evolve_batched": ([I, I, P, I, D, D, I, I, P, P, P, P, P, P], I),
+    "fq_qaoa_evolve_batched_levels": ([I, I, P, I, D, D, I, I, I, P, P, P, P, P, P], I),
     "fq_plan_x_passes": ([I, I, ctypes.POINTER(FqLayer), I], I),
     "fq_set_option": ([ctypes.c_char_p, I], I),
     "fq_last_passes": ([P, P, I], I),
@@ -126,14 +127,26 @@ def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
 
 
+_cuda_ok = False  # a CUDA device was found once (it does not go away within a process)
+_devices: dict[int, torch.device] = {}
+
+
 def device() -> torch.device:
-    """The CUDA device the simulator runs on; raises if none (no CPU fallback)."""
-    if not torch.cuda.is_available():
-        raise RuntimeError(
-            "paper_2309_04841_b200 needs a CUDA device (B200, sm_100a); "
-            "there is no CPU fallback"
-        )
-    return torch.device("cuda", torch.cuda.current_device())
+    """The CUDA device the simulator runs on; raises if none (no CPU fallback).
+    On the path of every call: the availability probe runs once per process."""
+    global _cuda_ok
+    if not _cuda_ok:
+        if not torch.cuda.is_available():
+            raise RuntimeError(
+                "paper_2309_04841_b200 needs a CUDA device (B200, sm_100a); "
+                "there is no CPU fallback"
+            )
+        _cuda_ok = True
+    idx = torch.cuda.current_device()
+    dev = _devices.get(idx)
+    if dev is None:
+        dev = _devices[idx] = torch.device("cuda", idx)
+    return dev
 
 
 def stream() -> int:
@@ -144,11 +157,11 @@ _scratch: dict[int, torch.Tensor] = {}
 
 
 def scratch() -> torch.Tensor:
-    dev = device()
-    buf = _scratch.get(dev.index)
+    idx = device().index
+    buf = _scratch.get(idx)
     if buf is None:
-        buf = torch.zeros(FQ_SCRATCH_DOUBLES, dtype=torch.float64, device=dev)
-        _scratch[dev.index] = buf
+        buf = torch.zeros(FQ_SCRATCH_DOUBLES, dtype=torch.float64, device=_devices[idx])
+        _scratch[idx] = buf
     return buf
 
 

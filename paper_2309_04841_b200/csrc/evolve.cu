@@ -58,6 +58,7 @@ struct ResParams {
     double *exp_out;        // [batch], nullable
     double init_amp;
     int n, p, mixer, init, apply_phase_mask_all;
+    int table_hi;           // k_resident16, uint16 costs: rows of the high phase table (0: sincos)
     int n_gates;
     unsigned char gates[kResMaxGates][2];
     // per (batch row, layer) angles: gam[b*p + l], bet[b*p + l]; row b = blockIdx.x
@@ -154,6 +155,166 @@ __global__ void __launch_bounds__(kResThreads) k_resident(const __grid_constant_
     if (P.psi_out) {
         double2 *dst = P.psi_out + (long long)b * N;
         for (int k = tid; k < N; k += kResThreads) dst[k] = st[k];
+    }
+}
+
+// ---------------------------------------------------------------- resident, register rounds (n <= 12, X / custom)
+// The whole state is ONE 2^12 tile of k_pass16 (qubit q = tile bit q; for
+// n < 12 the tile bits >= n carry zero amplitudes that are never stored):
+// 256 threads x 16 amplitudes in registers, a layer = phase + three radix-16
+// rounds over the register quads (8-11 | 0-3 | 4-7, walked forward on even
+// layers and backward on odd ones, so consecutive layers share a pattern and
+// a layer costs two shared-memory transposes), instead of k_resident's one
+// shared-memory sweep + barrier per qubit.  One CTA runs a whole program, so
+// the kernel is latency- and instruction-fetch-bound: the code is kept small
+// (one mixer per instantiation, one loop body for every register pattern,
+// the sincos phase out of line).
+constexpr int kRes16Smem = (kTilePadded + (kTableLo + kMaxTableHi) * 8) * (int)sizeof(double2);
+
+// Register pattern at run time (the layer loop is one small body for every
+// pattern): element index of register i = ibase + i * istep, padded
+// transpose slot = sbase + i * sstep, register bit j = qubit first + j.
+struct Res16Pat {
+    int ibase, istep, sbase, sstep, first;
+};
+__device__ __forceinline__ Res16Pat res16_pat(int pat, int tid) {
+    Res16Pat r;
+    if (pat == PAT8) {
+        r.ibase = tid; r.istep = 256; r.sbase = pat_base<PAT8>(tid); r.sstep = pat_step<PAT8>(1); r.first = 8;
+    } else if (pat == PAT0) {
+        r.ibase = tid << 4; r.istep = 1; r.sbase = pat_base<PAT0>(tid); r.sstep = pat_step<PAT0>(1); r.first = 0;
+    } else {
+        r.ibase = (tid & 15) | ((tid >> 4) << 8); r.istep = 16; r.sbase = pat_base<PAT4>(tid);
+        r.sstep = pat_step<PAT4>(1); r.first = 4;
+    }
+    return r;
+}
+
+// e^{-i gamma c_e}, float64 cost or a uint16 level without tables (out of line)
+template <int COST>
+static __device__ __noinline__ double2 res16_phase_sincos(const ResParams &P, int e, double gamma) {
+    double c;
+    if (COST == FQ_COST_F64) c = static_cast<const double *>(P.costs)[e];
+    else c = decode_u16(static_cast<const uint16_t *>(P.costs)[e], P.cost_scale, P.cost_offset);
+    return phase_f64(c, gamma);
+}
+
+template <int COST, int MIX>
+__global__ void __launch_bounds__(kThreads, 2) k_resident16(const __grid_constant__ ResParams P,
+                                                            const double *__restrict__ su2) {
+    extern __shared__ __align__(16) unsigned char res_smem[];
+    double2 *tile = reinterpret_cast<double2 *>(res_smem);
+    double2 *tlo = tile + kTilePadded;
+    double2 *thi = tlo + kTableLo * 8;
+    __shared__ double red[kThreads / 32];
+    const int tid = threadIdx.x, N = 1 << P.n, b = blockIdx.x;
+    const int table_hi = COST == FQ_COST_U16 ? P.table_hi : 0;
+    double2 v[kRegs];
+    Res16Pat cur = res16_pat(PAT8, tid);
+    const double2 *src = (P.init || P.psi_in == nullptr) ? nullptr : P.psi_in + (long long)b * P.in_stride;
+#pragma unroll
+    for (int i = 0; i < kRegs; ++i) {
+        const int e = cur.ibase + i * cur.istep;
+        v[i] = e >= N ? make_double2(0.0, 0.0) : src ? src[e] : make_double2(P.init_amp, 0.0);
+    }
+    int pat = PAT8;
+#pragma unroll 1
+    for (int l = 0; l < P.p; ++l) {
+        const double gamma = P.gam[b * P.p + l];
+        if (P.phase_on[l] && gamma != 0.0) {
+            if (COST == FQ_COST_U16 && table_hi > 0) {
+                // the previous layer's lookups are behind its transposes' barriers
+                build_phase_tables<double>(tlo, thi, table_hi, gamma, P.cost_scale, P.cost_offset);
+                __syncthreads();
+            }
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i) {
+                const int e = cur.ibase + i * cur.istep;
+                if (e >= N) continue;
+                double2 f;
+                if (COST == FQ_COST_U16 && table_hi > 0) {
+                    const unsigned raw = static_cast<const uint16_t *>(P.costs)[e];
+                    f = cmul(thi[(raw >> 6) * 8 + (tid & 7)], tlo[(raw & 63) * 8 + (tid & 7)]);
+                } else {
+                    f = res16_phase_sincos<COST>(P, e, gamma);
+                }
+                v[i] = cmul(v[i], f);
+            }
+        }
+        const int qlo = P.qlo[l], qhi = P.qhi[l];
+        // RX in the tiled passes' form: f (1, tan b) or f (cot b, 1), two DFMA per
+        // amplitude and qubit, the layer's f^targets applied once at its end
+        double rc = 0.0, f = 1.0;
+        int mode = 0;
+        if (MIX == MIX_RX) {
+            double s, c;
+            sincos(P.bet[b * P.p + l], &s, &c);
+            if (fabs(c) >= fabs(s)) { rc = s / c; f = c; }
+            else { mode = 1; rc = c / s; f = s; }
+        }
+        // three rounds: 8 -> 0 -> 4 from PAT8, 4 -> 0 -> 8 from PAT4
+#pragma unroll 1
+        for (int r = 0; r < 3; ++r) {
+            if (r > 0) {
+                const int next = r == 1 ? PAT0 : (pat == PAT0 ? (l & 1 ? PAT8 : PAT4) : pat);
+                const Res16Pat nx = res16_pat(next, tid);
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) tile[cur.sbase + i * cur.sstep] = v[i];
+                __syncthreads();
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) v[i] = tile[nx.sbase + i * nx.sstep];
+                __syncthreads();
+                cur = nx;
+                pat = next;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int q = cur.first + j;
+                if (q < qlo || q >= qhi) continue;
+                if constexpr (MIX == MIX_RX) {
+                    if (mode == 0) {
+#pragma unroll
+                        for (int i = 0; i < kRegs; ++i)
+                            if (!(i & (1 << j))) bfly_rx0(v[i], v[i | (1 << j)], rc);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < kRegs; ++i)
+                            if (!(i & (1 << j))) bfly_rx1(v[i], v[i | (1 << j)], rc);
+                    }
+                } else {
+                    const double *c4 = su2 + ((long long)l * P.n + q) * 4;
+                    const double2 a = make_double2(c4[0], c4[1]), bb = make_double2(c4[2], c4[3]);
+#pragma unroll
+                    for (int i = 0; i < kRegs; ++i)
+                        if (!(i & (1 << j))) bfly_su2(v[i], v[i | (1 << j)], a, bb);
+                }
+            }
+        }
+        if (MIX == MIX_RX) {
+            double fs = 1.0;
+            for (int q = max(qlo, 0); q < min(qhi, P.n); ++q) fs *= f;
+#pragma unroll
+            for (int i = 0; i < kRegs; ++i) v[i] = make_double2(v[i].x * fs, v[i].y * fs);
+        }
+    }
+    // objective and state in the final pattern
+    double acc = 0.0;
+    double2 *dst = P.psi_out ? P.psi_out + (long long)b * N : nullptr;
+#pragma unroll
+    for (int i = 0; i < kRegs; ++i) {
+        const int e = cur.ibase + i * cur.istep;
+        if (e >= N) continue;
+        if (P.exp_out) {
+            const double cv = (COST == FQ_COST_F64) ? static_cast<const double *>(P.costs)[e]
+                                                    : decode_u16(static_cast<const uint16_t *>(P.costs)[e],
+                                                                 P.cost_scale, P.cost_offset);
+            acc += cv * (v[i].x * v[i].x + v[i].y * v[i].y);
+        }
+        if (dst) dst[e] = v[i];
+    }
+    if (P.exp_out) {
+        const double t = block_sum<kThreads>(acc, red);
+        if (tid == 0) P.exp_out[b] = t;
     }
 }
 
@@ -996,8 +1157,31 @@ static int run_xy_program(const fq_evolve_desc *d, cudaStream_t st) {
     return FQ_OK;
 }
 
+static int g_res16 = 1;  // n <= 12, X / custom mixers: the register-round resident kernel (k_resident16)
+
+// uint16 levels -> rows of the high phase table (0: too many levels, sincos per amplitude)
+static int table_rows(int cost_levels) {
+    if (cost_levels <= 0) return 0;
+    const int rows = ((cost_levels - 1) >> 6) + 1;
+    return rows <= kMaxTableHi ? rows : 0;
+}
+
 template <int COST>
 static int launch_resident(const ResParams &P, int batch, const double *su2_dev, cudaStream_t st) {
+    if (g_res16 && (P.mixer == FQ_MIXER_X || P.mixer == FQ_MIXER_CUSTOM)) {
+        static bool configured16 = false;
+        if (!configured16) {
+            cudaFuncSetAttribute(k_resident16<COST, MIX_RX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRes16Smem);
+            cudaFuncSetAttribute(k_resident16<COST, MIX_SU2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRes16Smem);
+            configured16 = true;
+        }
+        const int th = COST == FQ_COST_U16 ? P.table_hi : 0;
+        const size_t smem16 = (size_t)(kTilePadded + (kTableLo + th) * 8) * sizeof(double2);
+        if (P.mixer == FQ_MIXER_X) k_resident16<COST, MIX_RX><<<batch, kThreads, smem16, st>>>(P, su2_dev);
+        else k_resident16<COST, MIX_SU2><<<batch, kThreads, smem16, st>>>(P, su2_dev);
+        FQ_LAUNCHED("k_resident16");
+        return FQ_OK;
+    }
     const size_t smem = (size_t)(1 << P.n) * sizeof(double2);
     static bool configured = false;
     if (!configured) {
@@ -1047,6 +1231,7 @@ static int run_resident_program(const fq_evolve_desc *d, cudaStream_t st) {
         P->psi_out = static_cast<double2 *>(d->psi);
         const bool last = (l0 + chunk >= d->n_layers);
         P->exp_out = last ? d->expectation_dev : nullptr;
+        P->table_hi = d->cost_kind == FQ_COST_U16 && g_phase_tables ? table_rows(d->cost_levels) : 0;
         for (int i = 0; i < cnt; ++i) {
             P->gam[i] = d->layers[l0 + i].gamma;
             P->bet[i] = d->layers[l0 + i].beta;
@@ -1170,6 +1355,7 @@ int fq_set_option(const char *name, int value) {
         {"phase_tables", &g_phase_tables, 0, 1},  // uint16 phase via smem tables (else sincos)
         {"plan", &g_plan, -1, 1},           // group plan: -1 cost model, 0 legacy, 1 small fusion groups
         {"plan_tmax", &g_plan_tmax, 0, 12},  // force the high-group chunk size (0: cost model)
+        {"res16", &g_res16, 0, 1},          // n <= 12 X / custom: register-round resident kernel
         {"sweep", &g_sweep, 0, 1},          // L2-resident slab sweeps of pass pairs
         {"sweep_team", &g_sweep_team, 1, 256},  // CTAs per sweep team
         {"sweep_slab_log2", &g_sweep_slab_log2, 16, 30},  // largest sweep slab, log2 bytes
@@ -1264,6 +1450,13 @@ int fq_last_passes(int *info, float *ms, int max) {
 int fq_qaoa_evolve_batched(int n, int mixer, const void *costs, int cost_kind, double scale, double offset, int p,
                            int batch, const double *gammas, const double *betas, const void *psi_init, void *psi_out,
                            double *out_dev, void *stream) {
+    return fq_qaoa_evolve_batched_levels(n, mixer, costs, cost_kind, scale, offset, 0, p, batch, gammas, betas,
+                                         psi_init, psi_out, out_dev, stream);
+}
+
+int fq_qaoa_evolve_batched_levels(int n, int mixer, const void *costs, int cost_kind, double scale, double offset,
+                                  int cost_levels, int p, int batch, const double *gammas, const double *betas,
+                                  const void *psi_init, void *psi_out, double *out_dev, void *stream) {
     FQ_CHECK_ARG(n >= 1 && n <= kTileBits, "fq_qaoa_evolve_batched: n=%d must be in [1, %d]", n, kTileBits);
     FQ_CHECK_ARG(costs && out_dev && batch >= 1 && p >= 0 && gammas && betas, "fq_qaoa_evolve_batched: bad args");
     FQ_CHECK_ARG(mixer != FQ_MIXER_CUSTOM, "fq_qaoa_evolve_batched: custom mixers are not batched");
@@ -1283,6 +1476,7 @@ int fq_qaoa_evolve_batched(int n, int mixer, const void *costs, int cost_kind, d
     P->in_stride = 0;
     P->psi_out = static_cast<double2 *>(psi_out);
     P->exp_out = out_dev;
+    P->table_hi = cost_kind == FQ_COST_U16 && g_phase_tables ? table_rows(cost_levels) : 0;
     fill_gates(*P, n, mixer);
     for (int l = 0; l < p; ++l) {
         P->phase_on[l] = 1;

@@ -285,8 +285,9 @@ class QaoaSimulator:
         for s in range(0, batch, chunk):
             e = min(batch, s + chunk)
             gs, bs = np.ascontiguousarray(g[s:e]), np.ascontiguousarray(b[s:e])
-            _lib.call("fq_qaoa_evolve_batched", self.n, _lib.MIXER_CODES[self.mixer.kind], cp, kind, scale, offset,
-                      p, e - s, gs.ctypes.data, bs.ctypes.data, None, None, out[s:].data_ptr(), _lib.stream())
+            levels = self._dc.levels if kind == _lib.COST_U16 else 0
+            _lib.call("fq_qaoa_evolve_batched_levels", self.n, _lib.MIXER_CODES[self.mixer.kind], cp, kind, scale,
+                      offset, levels, p, e - s, gs.ctypes.data, bs.ctypes.data, None, None, out[s:].data_ptr(), _lib.stream())
         return out.cpu().numpy()
 
     def get_statevector(self, result: QaoaResult) -> np.ndarray:
