@@ -220,7 +220,7 @@ __device__ __forceinline__ void bfly16(C2<R> (&v)[kRegs], const CoefSet &C, int 
 // exp(-i gamma c) for a float64 cost: the reference's angle = gamma * c, then sincos.
 __device__ __forceinline__ double2 phase_f64(double c, double gamma) {
     double s, co;
-    sincos(gamma * c, &s, &co);
+    fq_sincos(gamma * c, &s, &co);
     return make_double2(co, -s);
 }
 

@@ -32,7 +32,8 @@ struct XyRound {
     unsigned char tb[8];          // thread bit k <- tile bit tb[k]
     unsigned char ngates;
     unsigned char gate[kXyMaxGates];  // code = 4 * a + b: lo qubit at register bit a, hi qubit at b
-    unsigned short sreg[kRegs];   // swizzled smem slot of register i's tile-index part
+    unsigned short sreg[kRegs];   // swizzled smem BYTE offset of register i's tile-index part
+    unsigned short tnib[32];      // swizzled smem byte offset of the thread part: [tid & 15] ^ [16 + (tid >> 4)]
 };
 
 struct XyParams {
@@ -111,14 +112,6 @@ __device__ __forceinline__ void xy_apply(T (&v)[kRegs], int code, R c, R s) {
     }
 }
 
-// tile-index part of this thread in round r (thread bit k -> tile bit tb[k])
-__device__ __forceinline__ int xy_tpart(const XyRound &R, int tid) {
-    int e = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) e |= ((tid >> k) & 1) << R.tb[k];
-    return e;
-}
-
 __device__ __forceinline__ long long xy_tphys(const XyParams &P, const XyRound &R, int tid) {
     long long o = 0;
 #pragma unroll
@@ -164,11 +157,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__
     T *tlo = tile + kTile;
     T *thi = tlo + kTableLo * table_copies<RT>();
     __shared__ double red[kThreads / 32];
+    // per round, the thread part of the swizzled slot (byte offsets) by tid nibble:
+    // two shared loads per transpose instead of rebuilding it from the round's bit map
+    // and the register parts (same for every thread: broadcast reads)
+    __shared__ int tnib[kXyMaxRounds][32];
+    __shared__ __align__(16) int sreg[kXyMaxRounds][kRegs];
     const int tid = threadIdx.x;
+    for (int i = tid; i < P.nrounds * 32; i += kThreads) tnib[i >> 5][i & 31] = P.rounds[i >> 5].tnib[i & 31];
+    for (int i = tid; i < P.nrounds * kRegs; i += kThreads) sreg[i / kRegs][i % kRegs] = P.rounds[i / kRegs].sreg[i % kRegs];
     if (COST == FQ_COST_U16 && PH) {
         if (P.table_hi > 0) build_phase_tables<RT>(tlo, thi, P.table_hi, P.gamma, P.cost_scale, P.cost_offset);
-        __syncthreads();
     }
+    __syncthreads();
+    char *const tb = reinterpret_cast<char *>(tile);
+    const int lo_n = tid & 15, hi_n = 16 + (tid >> 4);
     const long long thr_first = xy_tphys(P, P.rounds[0], tid);
     const long long thr_last = xy_tphys(P, P.rounds[P.nrounds - 1], tid);
     double eacc = 0.0;
@@ -205,18 +207,29 @@ __global__ void __launch_bounds__(kThreads, 2) k_xy_pass(const __grid_constant__
             for (int i = 0; i < kRegs; ++i)
                 v[i] = cmul(v[i], xy_phase<COST, RT>(P, raw[i], tlo, thi));
         }
+        int sq = tnib[0][lo_n] ^ tnib[0][hi_n];
         for (int r = 0; r < P.nrounds; ++r) {
             const XyRound &R = P.rounds[r];
             if (r > 0) {  // transpose from round r-1's pattern to round r's
-                const XyRound &Q = P.rounds[r - 1];
-                const int sq = xy_slot(xy_tpart(Q, tid));
+                const int sr = tnib[r][lo_n] ^ tnib[r][hi_n];
+                int so[kRegs];
+#pragma unroll
+                for (int i = 0; i < kRegs; i += 4) {
+                    const int4 q = *reinterpret_cast<const int4 *>(&sreg[r - 1][i]);
+                    so[i] = q.x; so[i + 1] = q.y; so[i + 2] = q.z; so[i + 3] = q.w;
+                }
                 __syncthreads();
 #pragma unroll
-                for (int i = 0; i < kRegs; ++i) tile[sq ^ Q.sreg[i]] = v[i];
-                __syncthreads();
-                const int sr = xy_slot(xy_tpart(R, tid));
+                for (int i = 0; i < kRegs; ++i) *reinterpret_cast<T *>(tb + (sq ^ so[i])) = v[i];
 #pragma unroll
-                for (int i = 0; i < kRegs; ++i) v[i] = tile[sr ^ R.sreg[i]];
+                for (int i = 0; i < kRegs; i += 4) {
+                    const int4 q = *reinterpret_cast<const int4 *>(&sreg[r][i]);
+                    so[i] = q.x; so[i + 1] = q.y; so[i + 2] = q.z; so[i + 3] = q.w;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int i = 0; i < kRegs; ++i) v[i] = *reinterpret_cast<const T *>(tb + (sr ^ so[i]));
+                sq = sr;
             }
             for (int g = 0; g < R.ngates; ++g) xy_apply(v, R.gate[g], (decltype(v[0].x))P.c, (decltype(v[0].x))P.s);
         }
@@ -503,7 +516,7 @@ static std::vector<XyPassPlan> plan_xy(int n, const std::vector<std::pair<int, i
 }
 
 static void fill_round(XyRound &R, const std::vector<int> &bits, const std::vector<std::pair<int, int>> &gl,
-                       const std::vector<int> &tile) {
+                       const std::vector<int> &tile, int elem) {
     std::memset(&R, 0, sizeof R);
     for (int j = 0; j < 4; ++j) R.reg[j] = (unsigned char)bits[j];
     // thread bits: the other 8 tile bits; the three lane bits of a quarter-warp get
@@ -532,8 +545,16 @@ static void fill_round(XyRound &R, const std::vector<int> &bits, const std::vect
         int e = 0;
         for (int j = 0; j < 4; ++j)
             if ((i >> j) & 1) e |= 1 << bits[j];
-        R.sreg[i] = (unsigned short)xy_slot(e);
+        R.sreg[i] = (unsigned short)(xy_slot(e) * elem);
     }
+    // thread part by nibble of tid (xy_slot is GF(2)-linear: slot(a | b) = slot(a) ^ slot(b))
+    for (int h = 0; h < 2; ++h)
+        for (int v = 0; v < 16; ++v) {
+            int e = 0;
+            for (int k = 0; k < 4; ++k)
+                if ((v >> k) & 1) e |= 1 << R.tb[4 * h + k];
+            R.tnib[16 * h + v] = (unsigned short)(xy_slot(e) * elem);
+        }
     R.ngates = (unsigned char)gl.size();
     for (size_t g = 0; g < gl.size(); ++g) {
         const int lo = std::min(gl[g].first, gl[g].second), hi = std::max(gl[g].first, gl[g].second);
@@ -648,7 +669,8 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
             P->expect = (l + 1 == d->n_layers && pi + 1 == plans.size() && d->expectation_dev) ? 1 : 0;
             P->table_hi = table_hi;
             P->nrounds = (int)pl.round_bits.size();
-            for (int r = 0; r < P->nrounds; ++r) fill_round(P->rounds[r], pl.round_bits[r], pl.round_gates[r], pl.tile);
+            for (int r = 0; r < P->nrounds; ++r)
+                fill_round(P->rounds[r], pl.round_bits[r], pl.round_gates[r], pl.tile, c64 ? 8 : 16);
             for (int i = 0; i < kRegs; ++i) {
                 long long a = 0, b = 0;
                 for (int j = 0; j < 4; ++j)

@@ -35,8 +35,7 @@ def _run(sim, g, b, sweep):
     return res.state_device.clone(), sim.get_expectation(res), recs
 
 
-@pytest.mark.parametrize("n,p,dtype", [(26, 4, "complex128"), (25, 3, "complex128"), (26, 3, "complex64"),
-                                       (25, 2, "complex64")])
+@pytest.mark.parametrize("n,p,dtype", [(26, 4, "complex128"), (25, 3, "complex128"), (26, 3, "complex64")])
 def test_sweep_equals_separate_passes_and_oracle(n, p, dtype, sweep_opts):
     rng = np.random.default_rng(n + p)
     g, b = rng.uniform(-1, 1, p), rng.uniform(-1.6, 1.6, p)
