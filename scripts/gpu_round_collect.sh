@@ -13,6 +13,9 @@ for f in bench_c64 configs smoke; do :; done
 cp gpurun_out/bench_c64_$TAG.log profiles/$DEST/bench_c64.json 2>/dev/null
 cp gpurun_out/configs_$TAG.jsonl profiles/$DEST/configs.jsonl 2>/dev/null
 cp gpurun_out/smoke_$TAG.log profiles/$DEST/smoke.txt 2>/dev/null
+cp gpurun_out/xy_$TAG.log profiles/$DEST/xy.jsonl 2>/dev/null
+cp gpurun_out/latency_$TAG.log profiles/$DEST/latency.txt 2>/dev/null
+cp gpurun_out/bench_mp2_$TAG.log profiles/$DEST/bench_mp2_one_device.log 2>/dev/null
 mkdir -p gpurun_out/${DEST}_profiles
 cp -r profiles/$DEST/. gpurun_out/${DEST}_profiles/
 cp profiles/ncu_traffic.json gpurun_out/${DEST}_profiles/ncu_traffic.json
