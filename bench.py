@@ -142,6 +142,18 @@ def cpu_eval_rate(costs, p, g, b, layers_sample):
     return 1.0 / t_eval, t_layers, t_exp
 
 
+def cpu_model() -> str:
+    """Host CPU model (for the CPU baseline's provenance)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
@@ -177,7 +189,8 @@ def run_reference(args, rank):
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": f"LABS n={n} p={p} X-mixer complex128 objective evaluation", "n": n, "p": p,
                    "step": "one QAOA layer", "l2": "state > L2"},
-        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port", "sample": sample,
+                         "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "precompute_s": t_pre, "ms_per_layer": 1e3 * t_layer, "ms_expectation": 1e3 * t_exp,
     }
@@ -271,12 +284,21 @@ def run_config5(args, world, rank, k, barrier):
     g, b = angles(p)
     try:
         free, _ = torch.cuda.mem_get_info()
+        if os.environ.get("FQ_BENCH_ONE_DEVICE") == "1":
+            free //= world  # validation mode: every rank shares one device
         c64 = world == 1
         elem = 8 if c64 else 16
         n_local = n - k
-        if (1 << n_local) * (elem + 2) > 0.92 * free:
+        fits = (1 << n_local) * (elem + 2) <= 0.92 * free
+        if world > 1:  # every rank takes the same branch (the constructor below is collective)
+            import torch.distributed as dist
+
+            flag = torch.tensor([1 if fits else 0], dtype=torch.int32, device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            fits = bool(flag.item())
+        if not fits:
             return {"skipped": f"n=34 needs {(1 << n_local) * (elem + 2) / 2**30:.0f} GiB per GPU, "
-                               f"{free / 2**30:.0f} GiB free"}
+                               f"{free / 2**30:.0f} GiB free on this rank"}
         t0 = time.perf_counter()
         if world == 1:
             sim = QaoaSimulator(terms=labs_terms(n), dtype="complex64")
@@ -628,7 +650,7 @@ def main():
         costs_host = sim.get_cost_diagonal()
         layers_sample = 2
         rate, t_layer, t_exp = cpu_eval_rate(np.array(costs_host), p, g, b, layers_sample)
-        cpu = {"value": rate, "unit": "evals/s", "cores": O.num_threads(), "kind": "port",
+        cpu = {"value": rate, "unit": "evals/s", "cores": O.num_threads(), "kind": "port", "cpu": cpu_model(),
                "sample": f"{layers_sample} of {p} layers (phase + X mixer) + 1 expectation of LABS n={n} on the "
                          f"oracle C/OpenMP port, extrapolated to the p={p} evaluation "
                          f"({1e3 * t_layer:.0f} ms/layer, {1e3 * t_exp:.0f} ms expectation)"}

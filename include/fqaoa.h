@@ -205,6 +205,13 @@ typedef struct fq_evolve_desc {
  * whole program inside one CTA. */
 int fq_qaoa_evolve(const fq_evolve_desc *desc, void *stream);
 
+/* One objective evaluation, synchronous (the optimiser-loop call, reference
+ * qaoa_objective / QaoaSimulator.get_expectation(simulate_qaoa(...)),
+ * qaoa.py:137-149,185-194): fq_qaoa_evolve with desc->expectation_dev set,
+ * then the objective copied to *out_host and the stream synchronised — one
+ * ABI crossing per evaluation. */
+int fq_qaoa_objective(const fq_evolve_desc *desc, double *out_host, void *stream);
+
 /* Batched small-n evolution: `batch` independent parameter sets (gammas/betas
  * host arrays [batch][p]) for the same cost vector, each evolved from |+>^n
  * (or from psi_init if non-NULL, complex128[2^n] device) entirely on chip;

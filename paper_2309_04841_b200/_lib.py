@@ -68,6 +68,7 @@ _SIGS = {
     "fq_compact_u16": ([P, P, I64, D, D, P, P], I),
     "fq_rebase_u16": ([P, I64, I, P], I),
     "fq_qaoa_evolve": ([ctypes.POINTER(FqEvolveDesc), P], I),
+    "fq_qaoa_objective": ([ctypes.POINTER(FqEvolveDesc), ctypes.POINTER(D), P], I),
     "fq_qaoa_evolve_sharded": ([ctypes.POINTER(FqEvolveDesc), ctypes.POINTER(FqShardDesc), P], I),
     "fq_plan_sharded_passes": ([I, I, I, ctypes.POINTER(FqLayer), P], I),
     "fq_qaoa_evolve_batched": ([I, I, P, I, D, D, I, I, P, P, P, P, P, P], I),

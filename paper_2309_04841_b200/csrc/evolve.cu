@@ -318,6 +318,144 @@ __global__ void __launch_bounds__(kThreads, 2) k_resident16(const __grid_constan
     }
 }
 
+// 512 threads x 8 amplitudes: twice the warps of k_resident16 (a single CTA
+// is latency-bound), rounds over register triples (bits 9-11 | 0-2 | 3-5 |
+// 6-8, forward on even layers, backward on odd ones: three transposes per
+// layer).  Transpose slot e + (e >> 3): a quarter-warp's eight 16-B accesses
+// hit eight distinct bank groups in all four patterns.
+constexpr int kRes8Threads = 512;
+constexpr int kRes8Regs = 8;
+constexpr int kRes8Padded = kTile + kTile / 8;
+constexpr int kRes8Smem = (kRes8Padded + (kTableLo + kMaxTableHi) * 8) * (int)sizeof(double2);
+
+// register pattern k (k = 0..3): registers hold tile bits 3k..3k+2
+__device__ __forceinline__ Res16Pat res8_pat(int k, int tid) {
+    Res16Pat r;
+    const int lowm = (1 << (3 * k)) - 1;
+    r.ibase = (tid & lowm) | ((tid >> (3 * k)) << (3 * k + 3));
+    r.istep = 1 << (3 * k);
+    r.sbase = r.ibase + (r.ibase >> 3);
+    r.sstep = r.istep + (r.istep >> 3);
+    r.first = 3 * k;
+    return r;
+}
+
+template <int COST, int MIX>
+__global__ void __launch_bounds__(kRes8Threads, 1) k_resident8(const __grid_constant__ ResParams P,
+                                                               const double *__restrict__ su2) {
+    extern __shared__ __align__(16) unsigned char res_smem[];
+    double2 *tile = reinterpret_cast<double2 *>(res_smem);
+    double2 *tlo = tile + kRes8Padded;
+    double2 *thi = tlo + kTableLo * 8;
+    __shared__ double red[kRes8Threads / 32];
+    const int tid = threadIdx.x, N = 1 << P.n, b = blockIdx.x;
+    const int table_hi = COST == FQ_COST_U16 ? P.table_hi : 0;
+    double2 v[kRes8Regs];
+    int pat = 3;
+    Res16Pat cur = res8_pat(pat, tid);
+    const double2 *src = (P.init || P.psi_in == nullptr) ? nullptr : P.psi_in + (long long)b * P.in_stride;
+#pragma unroll
+    for (int i = 0; i < kRes8Regs; ++i) {
+        const int e = cur.ibase + i * cur.istep;
+        v[i] = e >= N ? make_double2(0.0, 0.0) : src ? src[e] : make_double2(P.init_amp, 0.0);
+    }
+#pragma unroll 1
+    for (int l = 0; l < P.p; ++l) {
+        const double gamma = P.gam[b * P.p + l];
+        if (P.phase_on[l] && gamma != 0.0) {
+            if (COST == FQ_COST_U16 && table_hi > 0) {
+                build_phase_tables<double>(tlo, thi, table_hi, gamma, P.cost_scale, P.cost_offset);
+                __syncthreads();
+            }
+#pragma unroll
+            for (int i = 0; i < kRes8Regs; ++i) {
+                const int e = cur.ibase + i * cur.istep;
+                if (e >= N) continue;
+                double2 f;
+                if (COST == FQ_COST_U16 && table_hi > 0) {
+                    const unsigned raw = static_cast<const uint16_t *>(P.costs)[e];
+                    f = cmul(thi[(raw >> 6) * 8 + (tid & 7)], tlo[(raw & 63) * 8 + (tid & 7)]);
+                } else {
+                    f = res16_phase_sincos<COST>(P, e, gamma);
+                }
+                v[i] = cmul(v[i], f);
+            }
+        }
+        const int qlo = P.qlo[l], qhi = P.qhi[l];
+        double rc = 0.0, f = 1.0;
+        int mode = 0;
+        if (MIX == MIX_RX) {
+            double sn, cs;
+            sincos(P.bet[b * P.p + l], &sn, &cs);
+            if (fabs(cs) >= fabs(sn)) { rc = sn / cs; f = cs; }
+            else { mode = 1; rc = cs / sn; f = sn; }
+        }
+        const int dir = l & 1;  // even layers 3 -> 0 -> 1 -> 2, odd layers 2 -> 1 -> 0 -> 3
+#pragma unroll 1
+        for (int r = 0; r < 4; ++r) {
+            if (r > 0) {
+                const int next = dir ? (r == 3 ? 3 : 2 - r) : r - 1;
+                const Res16Pat nx = res8_pat(next, tid);
+#pragma unroll
+                for (int i = 0; i < kRes8Regs; ++i) tile[cur.sbase + i * cur.sstep] = v[i];
+                __syncthreads();
+#pragma unroll
+                for (int i = 0; i < kRes8Regs; ++i) v[i] = tile[nx.sbase + i * nx.sstep];
+                __syncthreads();
+                cur = nx;
+                pat = next;
+            }
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const int q = cur.first + j;
+                if (q < qlo || q >= qhi) continue;
+                if constexpr (MIX == MIX_RX) {
+                    if (mode == 0) {
+#pragma unroll
+                        for (int i = 0; i < kRes8Regs; ++i)
+                            if (!(i & (1 << j))) bfly_rx0(v[i], v[i | (1 << j)], rc);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < kRes8Regs; ++i)
+                            if (!(i & (1 << j))) bfly_rx1(v[i], v[i | (1 << j)], rc);
+                    }
+                } else {
+                    const double *c4 = su2 + ((long long)l * P.n + q) * 4;
+                    const double2 a = make_double2(c4[0], c4[1]), bb = make_double2(c4[2], c4[3]);
+#pragma unroll
+                    for (int i = 0; i < kRes8Regs; ++i)
+                        if (!(i & (1 << j))) bfly_su2(v[i], v[i | (1 << j)], a, bb);
+                }
+            }
+        }
+        if (MIX == MIX_RX) {
+            double fs = 1.0;
+            for (int q = max(qlo, 0); q < min(qhi, P.n); ++q) fs *= f;
+#pragma unroll
+            for (int i = 0; i < kRes8Regs; ++i) v[i] = make_double2(v[i].x * fs, v[i].y * fs);
+        }
+    }
+    double acc = 0.0;
+    double2 *dst = P.psi_out ? P.psi_out + (long long)b * N : nullptr;
+#pragma unroll
+    for (int i = 0; i < kRes8Regs; ++i) {
+        const int e = cur.ibase + i * cur.istep;
+        if (e >= N) continue;
+        if (P.exp_out) {
+            const double cv = (COST == FQ_COST_F64) ? static_cast<const double *>(P.costs)[e]
+                                                    : decode_u16(static_cast<const uint16_t *>(P.costs)[e],
+                                                                 P.cost_scale, P.cost_offset);
+            acc += cv * (v[i].x * v[i].x + v[i].y * v[i].y);
+        }
+        if (dst) dst[e] = v[i];
+    }
+    if (P.exp_out) {
+        const double t = block_sum<kRes8Threads>(acc, red);
+        if (tid == 0) P.exp_out[b] = t;
+    }
+    (void)pat;
+}
+
 // ---------------------------------------------------------------- standalone phase (uint16)
 // T = double2 (complex128 states) or float2 (complex64); the angle is always fp64
 template <typename T>
@@ -1157,7 +1295,8 @@ static int run_xy_program(const fq_evolve_desc *d, cudaStream_t st) {
     return FQ_OK;
 }
 
-static int g_res16 = 1;  // n <= 12, X / custom mixers: the register-round resident kernel (k_resident16)
+static int g_res16 = 2;  // n <= 12, X / custom mixers: 0 one sweep per qubit (k_resident), 1 register rounds
+                         // of 16 amplitudes (k_resident16), 2 of 8 amplitudes x 512 threads (k_resident8)
 
 // uint16 levels -> rows of the high phase table (0: too many levels, sincos per amplitude)
 static int table_rows(int cost_levels) {
@@ -1168,7 +1307,21 @@ static int table_rows(int cost_levels) {
 
 template <int COST>
 static int launch_resident(const ResParams &P, int batch, const double *su2_dev, cudaStream_t st) {
-    if (g_res16 && (P.mixer == FQ_MIXER_X || P.mixer == FQ_MIXER_CUSTOM)) {
+    if (g_res16 == 2 && (P.mixer == FQ_MIXER_X || P.mixer == FQ_MIXER_CUSTOM)) {
+        static bool configured8 = false;
+        if (!configured8) {
+            cudaFuncSetAttribute(k_resident8<COST, MIX_RX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRes8Smem);
+            cudaFuncSetAttribute(k_resident8<COST, MIX_SU2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRes8Smem);
+            configured8 = true;
+        }
+        const int th = COST == FQ_COST_U16 ? P.table_hi : 0;
+        const size_t smem8 = (size_t)(kRes8Padded + (kTableLo + th) * 8) * sizeof(double2);
+        if (P.mixer == FQ_MIXER_X) k_resident8<COST, MIX_RX><<<batch, kRes8Threads, smem8, st>>>(P, su2_dev);
+        else k_resident8<COST, MIX_SU2><<<batch, kRes8Threads, smem8, st>>>(P, su2_dev);
+        FQ_LAUNCHED("k_resident8");
+        return FQ_OK;
+    }
+    if (g_res16 == 1 && (P.mixer == FQ_MIXER_X || P.mixer == FQ_MIXER_CUSTOM)) {
         static bool configured16 = false;
         if (!configured16) {
             cudaFuncSetAttribute(k_resident16<COST, MIX_RX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRes16Smem);
@@ -1298,6 +1451,15 @@ int fq_qaoa_evolve(const fq_evolve_desc *d, void *stream) {
     return run_x_program(d, st);
 }
 
+int fq_qaoa_objective(const fq_evolve_desc *d, double *out_host, void *stream) {
+    FQ_CHECK_ARG(d && out_host && d->expectation_dev, "fq_qaoa_objective: needs expectation_dev and out_host");
+    if (int s = fq_qaoa_evolve(d, stream)) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FQ_CUDA(cudaMemcpyAsync(out_host, d->expectation_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+    FQ_CUDA(cudaStreamSynchronize(st));
+    return FQ_OK;
+}
+
 int fq_qaoa_evolve_sharded(const fq_evolve_desc *d, const fq_shard_desc *s, void *stream) {
     FQ_CHECK_ARG(d && s, "fq_qaoa_evolve_sharded: null descriptor");
     FQ_CHECK_ARG(s->k >= 1 && s->k <= 3, "fq_qaoa_evolve_sharded: k=%d must be in [1, 3]", s->k);
@@ -1355,7 +1517,7 @@ int fq_set_option(const char *name, int value) {
         {"phase_tables", &g_phase_tables, 0, 1},  // uint16 phase via smem tables (else sincos)
         {"plan", &g_plan, -1, 1},           // group plan: -1 cost model, 0 legacy, 1 small fusion groups
         {"plan_tmax", &g_plan_tmax, 0, 12},  // force the high-group chunk size (0: cost model)
-        {"res16", &g_res16, 0, 1},          // n <= 12 X / custom: register-round resident kernel
+        {"res16", &g_res16, 0, 2},          // n <= 12 X / custom: resident kernel variant (2: k_resident8)
         {"sweep", &g_sweep, 0, 1},          // L2-resident slab sweeps of pass pairs
         {"sweep_team", &g_sweep_team, 1, 256},  // CTAs per sweep team
         {"sweep_slab_log2", &g_sweep_slab_log2, 16, 30},  // largest sweep slab, log2 bytes

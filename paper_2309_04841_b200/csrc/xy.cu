@@ -74,10 +74,14 @@ __device__ __forceinline__ const C *xy_cost(const XyParams &P, long long k) {
 }
 
 // XOR swizzle of a 12-bit tile index (bijective; GF(2)-linear, so the slot of
-// thread part | register part is the XOR of the parts' slots).  The bank group
-// of slot e is fold3(e): a quarter-warp whose three lane bits sit on tile bits
-// of distinct residues mod 3 is conflict-free.
+// thread part | register part is the XOR of the parts' slots).  16-B elements
+// (complex128): the bank group of slot e is fold3(e), and a quarter-warp whose
+// three lane bits sit on tile bits of distinct residues mod 3 is conflict-free.
+// 8-B elements (complex64): a half-warp is one 128-B wavefront, the bank pair
+// is fold4(e), and the four lane bits need distinct residues mod 4.
 __host__ __device__ __forceinline__ int xy_slot(int e) { return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7); }
+__host__ __device__ __forceinline__ int xy_slot8(int e) { return e ^ (((e >> 4) ^ (e >> 8)) & 15); }
+__host__ __device__ __forceinline__ int xy_slot_of(int e, int elem) { return elem == 8 ? xy_slot8(e) : xy_slot(e); }
 
 // x_lo' = c x_lo - i s x_hi ; x_hi' = -i s x_lo + c x_hi   (reference _kernels.py:44-47)
 template <int A, int B, typename T, typename R>
@@ -531,8 +535,9 @@ static void fill_round(XyRound &R, const std::vector<int> &bits, const std::vect
         order = rest;
     } else {
         std::vector<int> pool = rest;
-        for (int res = 0; res < 3; ++res) {
-            auto it = std::find_if(pool.begin(), pool.end(), [&](int b) { return b % 3 == res; });
+        const int mod = elem == 8 ? 4 : 3;  // lanes of one wavefront on distinct residues (see xy_slot)
+        for (int res = 0; res < mod; ++res) {
+            auto it = std::find_if(pool.begin(), pool.end(), [&](int b) { return b % mod == res; });
             if (it != pool.end()) {
                 order.push_back(*it);
                 pool.erase(it);
@@ -545,15 +550,15 @@ static void fill_round(XyRound &R, const std::vector<int> &bits, const std::vect
         int e = 0;
         for (int j = 0; j < 4; ++j)
             if ((i >> j) & 1) e |= 1 << bits[j];
-        R.sreg[i] = (unsigned short)(xy_slot(e) * elem);
+        R.sreg[i] = (unsigned short)(xy_slot_of(e, elem) * elem);
     }
-    // thread part by nibble of tid (xy_slot is GF(2)-linear: slot(a | b) = slot(a) ^ slot(b))
+    // thread part by nibble of tid (the swizzle is GF(2)-linear: slot(a | b) = slot(a) ^ slot(b))
     for (int h = 0; h < 2; ++h)
         for (int v = 0; v < 16; ++v) {
             int e = 0;
             for (int k = 0; k < 4; ++k)
                 if ((v >> k) & 1) e |= 1 << R.tb[4 * h + k];
-            R.tnib[16 * h + v] = (unsigned short)(xy_slot(e) * elem);
+            R.tnib[16 * h + v] = (unsigned short)(xy_slot_of(e, elem) * elem);
         }
     R.ngates = (unsigned char)gl.size();
     for (size_t g = 0; g < gl.size(); ++g) {

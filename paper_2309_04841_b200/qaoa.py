@@ -9,6 +9,7 @@ accessors return host (CPU) values, as in the paper's API.
 
 from __future__ import annotations
 
+import ctypes
 from collections import OrderedDict
 from dataclasses import dataclass
 from math import sqrt
@@ -236,6 +237,7 @@ class QaoaSimulator:
             raise ValueError(f"n={n} disagrees with problem size {self.n}")
         self.mixer = Mixer.parse(mixer)
         self._buffer: torch.Tensor | None = None
+        self._obj_ctx = None  # objective(): prepared descriptor for the last depth
 
     @property
     def device_costs(self) -> DeviceCosts:
@@ -263,9 +265,44 @@ class QaoaSimulator:
         """<C> of one parameter set — the optimiser-loop call (reference
         qaoa_objective, qaoa.py:185-194, bound to this simulator): the
         evolution runs in the simulator-owned state buffer and the objective
-        comes from the program's last pass; one host synchronisation."""
-        res = self.simulate_qaoa(gammas, betas, initial=initial, reuse_buffer=True)
-        return float(res.cached_expectation().item())
+        comes from the program's last pass; one host synchronisation.  X mixer
+        from |+>: one prepared descriptor per depth, one ABI call per
+        evaluation (fq_qaoa_objective: program, copy-out, synchronise)."""
+        if initial is not None or self.mixer.kind != "x":
+            res = self.simulate_qaoa(gammas, betas, initial=initial, reuse_buffer=True)
+            return float(res.cached_expectation().item())
+        gs, bs = tuple(float(g) for g in gammas), tuple(float(b) for b in betas)
+        if len(gs) != len(bs):
+            raise ValueError(f"{len(gs)} gammas but {len(bs)} betas")
+        ctx = self._obj_ctx
+        if ctx is None or ctx[0] != len(gs) or self._buffer is None:
+            if self._buffer is None:
+                self._buffer = torch.empty(1 << self.n, dtype=self.dtype, device=_lib.device())
+            p = len(gs)
+            arr = (_lib.FqLayer * max(1, p))()
+            exp_dev = torch.empty(1, dtype=torch.float64, device=self._buffer.device)
+            desc = _lib.FqEvolveDesc()
+            desc.psi = self._buffer.data_ptr()
+            desc.n = self.n
+            kind, cp, scale, offset = self._dc.kernel_view()
+            desc.cost_kind, desc.costs, desc.cost_scale, desc.cost_offset = kind, cp, scale, offset
+            desc.cost_levels = self._dc.levels if kind == _lib.COST_U16 else 0
+            desc.mixer = _lib.MIXER_CODES["x"]
+            desc.n_layers = p
+            desc.layers = arr
+            desc.init = 1
+            desc.init_amp = 1.0 / sqrt(float(1 << self.n))
+            desc.expectation_dev = exp_dev.data_ptr()
+            desc.scratch = _lib.scratch().data_ptr()
+            desc.state_kind = _lib.STATE_C64 if self.dtype == torch.complex64 else _lib.STATE_C128
+            ctx = self._obj_ctx = (p, arr, desc, exp_dev, ctypes.c_double(), _lib.load().fq_qaoa_objective)
+        _, arr, desc, _, out, fn = ctx
+        for i, (g, b) in enumerate(zip(gs, bs)):
+            L = arr[i]
+            L.gamma, L.beta, L.apply_phase, L.q_lo, L.q_hi = g, b, 1, 0, self.n
+        _lib.check(fn(ctypes.byref(desc), ctypes.byref(out), _lib.stream()), "fq_qaoa_objective")
+        increment_version(self._buffer)  # a reuse_buffer result's state was overwritten
+        return out.value
 
     def simulate_qaoa_batched(self, gammas, betas) -> np.ndarray:
         """Expectations of many parameter sets at once (n <= 12: each set

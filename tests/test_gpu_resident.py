@@ -99,3 +99,21 @@ def test_batched_vs_oracle(n, p):
     for i in range(0, 300, 37):
         ref = O.expectation(O.simulate(costs, G[i], B[i]), costs)
         assert got[i] == pytest.approx(ref, rel=1e-10, abs=1e-12)
+
+
+@pytest.mark.parametrize("n", [8, 12, 15])
+def test_objective_fast_path(n):
+    """QaoaSimulator.objective (one fq_qaoa_objective call per evaluation,
+    prepared descriptor per depth) equals get_expectation(simulate_qaoa(...))
+    and the oracle, across depth changes; mismatched angle lists raise like
+    QaoaParams."""
+    sim = QaoaSimulator(terms=labs_terms(n))
+    costs = sim.get_cost_diagonal()
+    rng = np.random.default_rng(n)
+    for p in (3, 5, 3, 1):
+        g, b = rng.uniform(-1, 1, p), rng.uniform(-1.6, 1.6, p)
+        e = sim.objective(g, b)
+        assert e == pytest.approx(sim.get_expectation(sim.simulate_qaoa(g, b)), rel=1e-12, abs=1e-13)
+        assert e == pytest.approx(O.expectation(O.simulate(costs, g, b), costs), rel=1e-10, abs=1e-12)
+    with pytest.raises(ValueError, match="gammas but"):
+        sim.objective([0.1, 0.2], [0.3])
