@@ -50,27 +50,38 @@ __device__ __forceinline__ double decode_u16(uint16_t v, double scale, double of
 // (__kernel_sin / __kernel_cos coefficients); |error| ~1e-16, against the
 // 1e-10 state tolerance of the reference's np.exp(-1j * gamma * c).  Larger
 // arguments take the library sincos.
+// coefficients in the constant bank: the FP64 instructions take them as c[][]
+// operands (double immediates would be rebuilt with uniform moves every use)
+__constant__ double kSinCosCoef[15] = {
+    0.63661977236758134308, 1.5707963267948966192, 6.1232339957367658e-17, -1.4973849048591698e-33,
+    1.58969099521155010221e-10, -2.50507602534068634195e-08, 2.75573137070700676789e-06,
+    -1.98412698298579493134e-04, 8.33333333332248946124e-03, -1.66666666666666324348e-01,
+    -1.13596475577881948265e-11, 2.08757232129817482790e-09, -2.75573143513906633035e-07,
+    2.48015872894767294178e-05, -1.38888888888741095749e-03};
+__constant__ double kCosC1 = 4.16666666666666019037e-02;
+
 __device__ __forceinline__ void fq_sincos(double x, double *sp, double *cp) {
     if (!(fabs(x) < 1.6e6)) {
         sincos(x, sp, cp);
         return;
     }
-    const double k = rint(x * 0.63661977236758134308);  // 2 / pi
-    double r = fma(-k, 1.5707963267948966192, x);
-    r = fma(-k, 6.1232339957367658e-17, r);
-    r = fma(-k, -1.4973849048591698e-33, r);
+    const double *K = kSinCosCoef;
+    const double k = rint(x * K[0]);  // 2 / pi
+    double r = fma(-k, K[1], x);
+    r = fma(-k, K[2], r);
+    r = fma(-k, K[3], r);
     const double z = r * r;
-    double ps = fma(z, 1.58969099521155010221e-10, -2.50507602534068634195e-08);
-    ps = fma(z, ps, 2.75573137070700676789e-06);
-    ps = fma(z, ps, -1.98412698298579493134e-04);
-    ps = fma(z, ps, 8.33333333332248946124e-03);
-    ps = fma(z, ps, -1.66666666666666324348e-01);
+    double ps = fma(z, K[4], K[5]);
+    ps = fma(z, ps, K[6]);
+    ps = fma(z, ps, K[7]);
+    ps = fma(z, ps, K[8]);
+    ps = fma(z, ps, K[9]);
     const double sn = fma(r * z, ps, r);
-    double pc = fma(z, -1.13596475577881948265e-11, 2.08757232129817482790e-09);
-    pc = fma(z, pc, -2.75573143513906633035e-07);
-    pc = fma(z, pc, 2.48015872894767294178e-05);
-    pc = fma(z, pc, -1.38888888888741095749e-03);
-    pc = fma(z, pc, 4.16666666666666019037e-02);
+    double pc = fma(z, K[10], K[11]);
+    pc = fma(z, pc, K[12]);
+    pc = fma(z, pc, K[13]);
+    pc = fma(z, pc, K[14]);
+    pc = fma(z, pc, kCosC1);
     const double cs = fma(z * z, pc, fma(-0.5, z, 1.0));
     const int q = (int)(long long)k & 3;
     const double s0 = (q & 1) ? cs : sn, c0 = (q & 1) ? sn : cs;
