@@ -94,7 +94,8 @@ _lock = threading.Lock()
 def load(path: str | None = None):
     """Load libfqaoa.so (no CUDA device needed to load).  FQ_LIB_VARIANT=<name>
     selects a development build of the same sources with other compile-time
-    options (scripts/build_variant.py, A/B timing only)."""
+    options (scripts/build_variant.py, A/B timing only); FQ_OPTIONS sets
+    run-time options (fq_set_option) at load."""
     global _lib
     with _lock:
         if _lib is None:
@@ -112,6 +113,12 @@ def load(path: str | None = None):
                 fn.argtypes = args
                 fn.restype = res
             _lib = lib
+            # development: FQ_OPTIONS="name=value,..." applies fq_set_option at load
+            # (A/B runs of the test suite under a kernel variant)
+            for item in filter(None, os.environ.get("FQ_OPTIONS", "").split(",")):
+                name, _, value = item.partition("=")
+                if lib.fq_set_option(name.strip().encode(), int(value)) != FQ_OK:
+                    raise ValueError(f"FQ_OPTIONS: {item}: {(lib.fq_last_error() or b'').decode()}")
     return _lib
 
 

@@ -670,9 +670,17 @@ static int target_mask(const Group &g) {
     return m;
 }
 
-static int pass_seq(const Group &g, const PlannedPass &pp) {
+// lane_ok (X mixer, shard-local group, option lane3): a group whose only target
+// among tile bits 0..3 is bit 3 runs the two-pattern programs with bit 3 as a
+// lane butterfly (K_LANE3)
+static int g_lane3 = 1;
+static int lane_bits(const Group &g, bool lane_ok) {
+    return lane_ok && g_lane3 && (target_mask(g) & 0xF) == 0x8 ? 0x8 : 0;
+}
+
+static int pass_seq(const Group &g, const PlannedPass &pp, bool lane_ok = false) {
     const bool heavy = pp.layerB >= 0 && pp.phase_layer >= 0 && pp.phase_at == 2;
-    const bool low_quad = (target_mask(g) & 0xF) != 0;
+    const bool low_quad = (target_mask(g) & 0xF) != 0 && !lane_bits(g, lane_ok);
     if (heavy) return low_quad ? SEQ_84048 : SEQ_848;
     return low_quad ? SEQ_840 : SEQ_84;
 }
@@ -715,12 +723,15 @@ static int global_count(const Group &g, int n, int kq) {
     return c;
 }
 
+// extra cost of the lane-shuffle butterflies of a K_LANE3 pass (light, heavy)
+static const double kLanePassCost[2] = {0.08, 0.16};
+
 // A peer-memory pass moves (K-1)/K of its bytes over NVLink (~0.9 TB/s per
 // direction vs ~6.5 TB/s of HBM).
 constexpr double kGlobalPassCost = 5.0;
 
 static double plan_cost(const std::vector<PlannedPass> &seq, const std::vector<Group> &gs, int n, int elem,
-                        int kq = 0) {
+                        int kq = 0, bool rx = true) {
     for (auto &g : gs) {
         const int c = global_count(g, n, kq);
         if (c != 0 && c != kq) return 1e300;
@@ -733,8 +744,10 @@ static double plan_cost(const std::vector<PlannedPass> &seq, const std::vector<G
             c += 1.0;
             continue;
         }
-        const int sq = pass_seq(gs[pp.group], pp);
+        const bool lane_ok = rx && global_count(gs[pp.group], n, kq) == 0;
+        const int sq = pass_seq(gs[pp.group], pp, lane_ok);
         double pc = pass_cost(sq) * (l2_resident ? 1.0 : run_factor((long long)elem << run_bits_of(gs[pp.group]), seq_heavy(sq)));
+        if (lane_bits(gs[pp.group], lane_ok)) pc += seq_heavy(sq) ? kLanePassCost[1] : kLanePassCost[0];
         // a spanning pass is NVLink-bound: its DRAM run lengths hide behind the link
         // (and its round program too: the link time is the same for every program)
         if (kq > 0 && global_count(gs[pp.group], n, kq) > 0) pc = std::max(pc, kGlobalPassCost);
@@ -745,7 +758,7 @@ static double plan_cost(const std::vector<PlannedPass> &seq, const std::vector<G
 
 // elem: bytes per amplitude (16 complex128, 8 complex64); kq: global qubits of a sharded state
 static std::vector<PlannedPass> plan_x_search(int n, int nl, const fq_layer *layers, std::vector<Group> &groups,
-                                              bool fuse, int elem, int kq) {
+                                              bool fuse, int elem, int kq, bool rx) {
     std::vector<PlannedPass> best;
     double best_cost = 1e300;
     if (g_plan >= 0 || g_plan_tmax > 0) {  // forced shape (style and / or chunk size); invalid -> search
@@ -754,7 +767,7 @@ static std::vector<PlannedPass> plan_x_search(int n, int nl, const fq_layer *lay
             const int tmax = g_plan_tmax > 0 ? g_plan_tmax : (style == 0 ? 10 : 8);
             std::vector<Group> gs;
             auto seq = plan_with(n, nl, layers, gs, style, tmax, fuse);
-            const double c = plan_cost(seq, gs, n, elem, kq);
+            const double c = plan_cost(seq, gs, n, elem, kq, rx);
             if (c < best_cost - 1e-9 && c < 1e299) {
                 best_cost = c;
                 best = seq;
@@ -767,7 +780,7 @@ static std::vector<PlannedPass> plan_x_search(int n, int nl, const fq_layer *lay
         for (int tmax = 12; tmax >= 4; --tmax) {
             std::vector<Group> gs;
             auto seq = plan_with(n, nl, layers, gs, style, tmax, fuse);
-            const double c = plan_cost(seq, gs, n, elem, kq);
+            const double c = plan_cost(seq, gs, n, elem, kq, rx);
             if (c < best_cost - 1e-9) {
                 best_cost = c;
                 best = seq;
@@ -789,11 +802,11 @@ struct PlanMemo {
 };
 
 static std::vector<PlannedPass> plan_x(int n, int nl, const fq_layer *layers, std::vector<Group> &groups, bool fuse,
-                                       int elem, int kq = 0) {
+                                       int elem, int kq = 0, bool rx = true) {
     static std::mutex mu;
     static std::vector<PlanMemo> memo;
     static size_t next = 0;
-    std::vector<long long> key = {n, nl, elem, kq, fuse ? 1 : 0, g_plan, g_plan_tmax};
+    std::vector<long long> key = {n, nl, elem, kq, fuse ? 1 : 0, g_plan, g_plan_tmax, rx ? 1 : 0, g_lane3};
     key.reserve(key.size() + 3 * (size_t)nl);
     for (int l = 0; l < nl; ++l) {
         key.push_back(layers[l].q_lo);
@@ -808,7 +821,7 @@ static std::vector<PlannedPass> plan_x(int n, int nl, const fq_layer *layers, st
                 return m.seq;
             }
     }
-    auto seq = plan_x_search(n, nl, layers, groups, fuse, elem, kq);
+    auto seq = plan_x_search(n, nl, layers, groups, fuse, elem, kq, rx);
     std::lock_guard<std::mutex> lock(mu);
     PlanMemo m{std::move(key), seq, groups};
     if (memo.size() < 32) memo.push_back(std::move(m));
@@ -828,10 +841,11 @@ static long long deposit(long long x, long long mask) {
 }
 
 // Mask class of a pass (template K of k_pass16) from its per-round masks.
-static int mask_class(int seq, const unsigned char *maskA) {
+static int mask_class(int seq, const unsigned char *maskA, int lane = 0) {
     const int nr = seq_rounds(seq);
     bool full = true;
     for (int r = 0; r < nr; ++r) full &= maskA[r] == 0xF;
+    if (lane) return full && lane == 0x8 && (seq == SEQ_84 || seq == SEQ_848) ? K_LANE3 : -1;
     if (full) return K_FULL;
     if (seq == SEQ_84 || seq == SEQ_848) {
         for (int k = 1; k <= 3; ++k) {
@@ -848,7 +862,11 @@ static int mask_class(int seq, const unsigned char *maskA) {
 // a light pass runs in the run-time form: it only occurs for gamma = 0 layers).
 static int launch_pass(int mix, int cost, bool c64, const PassParams &P, const PassMaps &M, int seq, int ph, int ma,
                        int mb, int grid, cudaStream_t st) {
-    const int k = mask_class(seq, P.maskA);
+    const int k = mask_class(seq, P.maskA, P.lane);
+    if (k < 0) {
+        set_error("launch_pass: lane butterflies on tile bits 0x%x are not supported", P.lane);
+        return FQ_ERR_UNSUPPORTED;
+    }
     if (mix == MIX_SU2)
         return c64 ? launch_pass_su2_c64(P, M, cost, seq, ph, mb == 2 ? 2 : 3, k, grid, st)
                    : launch_pass_su2(P, M, cost, seq, ph, mb == 2 ? 2 : 3, k, grid, st);
@@ -872,8 +890,8 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCt
     const bool c64 = d->state_kind == FQ_STATE_C64;
     const long long elem = c64 ? (long long)sizeof(float2) : (long long)sizeof(double2);
     const int CB = d->cost_kind == FQ_COST_F64 ? 8 : 2;
-    auto seq = plan_x(nv, d->n_layers, d->layers, groups, g_fuse != 0, (int)elem, kq);
     const int mix = (d->mixer == FQ_MIXER_X) ? MIX_RX : MIX_SU2;
+    auto seq = plan_x(nv, d->n_layers, d->layers, groups, g_fuse != 0, (int)elem, kq, mix == MIX_RX);
     const long long n_tiles = 1LL << (nl - kTileBits);  // per shard
     int table_hi = 0;
     if (d->cost_kind == FQ_COST_U16 && d->cost_levels > 0 && g_phase_tables) {
@@ -992,7 +1010,9 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCt
         P.expect = expect_ ? 1 : 0;
         const int tmask = target_mask(g);
         two = pp.layerB >= 0;
-        sq = pass_seq(g, pp);
+        const bool lane_ok = mix == MIX_RX && !global;
+        sq = pass_seq(g, pp, lane_ok);
+        P.lane = lane_bits(g, lane_ok);
         for (int r = 0; r < seq_rounds(sq); ++r)
             P.maskA[r] = P.maskB[r] = (unsigned char)((tmask >> pat_first_bit(seq_pat(sq, r))) & 15);
         ph = 0;
@@ -1055,6 +1075,7 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCt
         build(si, init_pending, false, P1, sq1, ph1, ma1, mb1, two1);
         build(si + 1, false, last2 && d->expectation_dev, P2, sq2, ph2, ma2, mb2, two2);
         if ((ph1 == 1 || ph1 == 2) && (ph2 == 1 || ph2 == 2)) return FQ_OK;
+        if (P1.lane || P2.lane) return FQ_OK;  // no sweep instantiation with lane butterflies
         SweepKind kind{sq1, ph1, ma1, mb1, mask_class(sq1, P1.maskA), sq2, ph2, ma2, mb2, mask_class(sq2, P2.maskA)};
         if (!sweep_supported(mix, d->cost_kind, c64, kind)) return FQ_OK;
         SweepParams *S = new SweepParams;
@@ -1180,7 +1201,7 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCt
             std::memset(&M, 0, sizeof M);
             const int ggrid = (int)std::min<long long>(P.n_tiles, (long long)sms * 2);
             P.step_dep = deposit(ggrid, P.tile_mask);
-            int k = mask_class(sq, P.maskA);
+            int k = mask_class(sq, P.maskA, P.lane);
             int mbv = (mix == MIX_RX && !seq_heavy(sq) && mb != 2) ? 3 : mb;
             if (mix == MIX_SU2) mbv = mb == 2 ? 2 : 3;
             const int s = c64 ? launch_pass_global_c64(d->cost_kind, P, M, sq, ph, ma, mbv, k, ggrid, st)
@@ -1517,6 +1538,7 @@ int fq_set_option(const char *name, int value) {
         {"phase_tables", &g_phase_tables, 0, 1},  // uint16 phase via smem tables (else sincos)
         {"plan", &g_plan, -1, 1},           // group plan: -1 cost model, 0 legacy, 1 small fusion groups
         {"plan_tmax", &g_plan_tmax, 0, 12},  // force the high-group chunk size (0: cost model)
+        {"lane3", &g_lane3, 0, 1},          // 9-target high groups: tile bit 3 as lane butterflies (K_LANE3)
         {"res16", &g_res16, 0, 2},          // n <= 12 X / custom: resident kernel variant (2: k_resident8)
         {"sweep", &g_sweep, 0, 1},          // L2-resident slab sweeps of pass pairs
         {"sweep_team", &g_sweep_team, 1, 256},  // CTAs per sweep team

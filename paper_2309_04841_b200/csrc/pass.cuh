@@ -80,6 +80,8 @@ struct PassParams {
     int pf_dist;              // L2 prefetch distance in grid strides (0: off)
     int run_bits;             // tile bits 0..run_bits-1 sit at physical bits 0..run_bits-1 (contiguous runs)
     int pf_cost;              // also prefetch the cost slice of the tile
+    int lane;                 // K_LANE3 programs: tile bits 0..3 (here only bit 3) that are targets, applied as
+                              // lane butterflies (warp shuffles) in the PAT4 rounds
     int sm_rank, sm_shift[5], sm_bits[5];  // state tensor map: rank, outer-dim coordinate = (t >> shift) & (2^bits - 1)
     int cm_rank, cm_shift[5], cm_bits[5];  // cost tensor map (cm_rank = 0: no cost prefetch)
     int probe;                // development: 1 no cost loads, 2 fixed table row, 4 no phase multiply
@@ -212,6 +214,26 @@ __device__ __forceinline__ void bfly16(C2<R> (&v)[kRegs], const CoefSet &C, int 
 #pragma unroll
             for (int i = 0; i < kRegs; ++i)
                 if (!(i & (1 << j))) bfly_su2(v[i], v[i | (1 << j)], a, b);
+        }
+    }
+}
+
+// RX butterflies on a lane bit: the partner amplitude sits in lane ^ LM; both
+// halves of the pair take the same form, own' = own - i t partner (M = 0) or
+// u own - i partner (M = 1), with the register butterflies' FMA order (bit-identical).
+template <int M, int LM, typename R>
+__device__ __forceinline__ void lane_bfly16(C2<R> (&v)[kRegs], const CoefSet &C) {
+    if constexpr (M == 3) {
+        if (C.mode == 0) lane_bfly16<0, LM, R>(v, C);
+        else lane_bfly16<1, LM, R>(v, C);
+        return;
+    } else {
+        const R r = (R)C.r;
+#pragma unroll
+        for (int i = 0; i < kRegs; ++i) {
+            const R px = __shfl_xor_sync(0xffffffffu, v[i].x, LM), py = __shfl_xor_sync(0xffffffffu, v[i].y, LM);
+            if (M == 0) v[i] = Cx<R>::make(fma(r, py, v[i].x), fma(-r, px, v[i].y));
+            else v[i] = Cx<R>::make(fma(r, v[i].x, py), fma(r, v[i].y, -px));
         }
     }
 }
@@ -360,11 +382,16 @@ __device__ __forceinline__ void prefetch_tile(const PassParams &P, const CUtenso
 // visited quad is all targets; K = 1..3 (SEQ_84 / SEQ_848 only): the PAT8 quad is
 // all targets and the PAT4 quad has its top K bits as targets (a high group of
 // 4 + K targets above 8 - K spectators).
-enum { K_RUNTIME = 0, K_FULL = 4 };
+// K = K_LANE3 (SEQ_84 / SEQ_848, X mixer): both quads all targets, and tile bit 3
+// too — in PAT4 it is lane bit 3, so its butterflies run across lanes (warp
+// shuffles) inside the PAT4 rounds: a 9-target high group (3 low spectators,
+// n >= 30) runs the two-pattern programs instead of 8|0|4 (one transpose less,
+// two less in the fused two-layer pass).
+enum { K_RUNTIME = 0, K_FULL = 4, K_LANE3 = 5 };
 template <int K, int SEQ>
 __device__ __forceinline__ int round_mask(const unsigned char *rt, int r) {
     if constexpr (K == K_RUNTIME) return rt[r];
-    else if constexpr (K == K_FULL) return 0xF;
+    else if constexpr (K == K_FULL || K == K_LANE3) return 0xF;
     else return seq_pat(SEQ, r) == PAT4 ? ((0xF << (4 - K)) & 0xF) : 0xF;
 }
 
@@ -483,7 +510,9 @@ __device__ __forceinline__ void pass_tile(const PassParams &P, long long base, C
                 if (HAS_B) bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 0));
                 transpose<PAT8, PAT4>(tile, v, tid);
                 bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+                if constexpr (K == K_LANE3) lane_bfly16<MA, 8, R>(v, P.A);
                 if (HAS_B) bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
+                if constexpr (K == K_LANE3 && HAS_B) lane_bfly16<MB, 8, R>(v, P.B);
             } else if constexpr (SEQ == SEQ_84048) {
                 transpose<PAT8, PAT0>(tile, v, tid);
                 bfly16<MIX, MA, PAT0, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
@@ -498,7 +527,9 @@ __device__ __forceinline__ void pass_tile(const PassParams &P, long long base, C
             } else {  // SEQ_848
                 transpose<PAT8, PAT4>(tile, v, tid);
                 bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
+                if constexpr (K == K_LANE3) lane_bfly16<MA, 8, R>(v, P.A);
                 phase_all();
+                if constexpr (K == K_LANE3) lane_bfly16<MB, 8, R>(v, P.B);
                 bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
                 transpose<PAT4, PAT8>(tile, v, tid);
                 bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
@@ -628,25 +659,31 @@ static int select_seq(const PassParams &P, const PassMaps &M, int ph, int ma, in
 #define FQ_K(PHV, MAV, MBV)                                                                                  \
     if (ph == PHV && ma == MAV && mb == MBV) {                                                               \
         if (k == K_FULL) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_FULL, R, G>(P, M, grid, st);   \
+        if constexpr (kHigh && MIX == MIX_RX && !G) {                                                        \
+            if (k == K_LANE3) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_LANE3, R, G>(P, M, grid, st); \
+        }                                                                                                    \
         if constexpr (kHigh && MIX == MIX_RX) {                                                              \
             if (k == 1) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 1, R, G>(P, M, grid, st);         \
             if (k == 2) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 2, R, G>(P, M, grid, st);         \
             if (k == 3) return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, 3, R, G>(P, M, grid, st);         \
         }                                                                                                    \
+        if (k == K_LANE3) break; /* lane butterflies have no run-time-mask form */                            \
         return launch_pass16<MIX, COST, SEQ, PHV, MAV, MBV, K_RUNTIME, R, G>(P, M, grid, st);                 \
     }
-    if constexpr (seq_heavy(SEQ)) {
-        if constexpr (MIX == MIX_RX) {
-            FQ_K(2, 0, 0) FQ_K(2, 0, 1) FQ_K(2, 1, 0) FQ_K(2, 1, 1)
+    do {
+        if constexpr (seq_heavy(SEQ)) {
+            if constexpr (MIX == MIX_RX) {
+                FQ_K(2, 0, 0) FQ_K(2, 0, 1) FQ_K(2, 1, 0) FQ_K(2, 1, 1)
+            } else {
+                FQ_K(2, 0, 3)
+            }
         } else {
-            FQ_K(2, 0, 3)
+            FQ_K(0, 0, 2) FQ_K(0, 0, 3) FQ_K(1, 0, 2) FQ_K(1, 0, 3) FQ_K(3, 0, 2)
+            if constexpr (MIX == MIX_RX) { FQ_K(0, 1, 2) FQ_K(0, 1, 3) FQ_K(1, 1, 2) FQ_K(1, 1, 3) FQ_K(3, 1, 2) }
         }
-    } else {
-        FQ_K(0, 0, 2) FQ_K(0, 0, 3) FQ_K(1, 0, 2) FQ_K(1, 0, 3) FQ_K(3, 0, 2)
-        if constexpr (MIX == MIX_RX) { FQ_K(0, 1, 2) FQ_K(0, 1, 3) FQ_K(1, 1, 2) FQ_K(1, 1, 3) FQ_K(3, 1, 2) }
-    }
+    } while (0);
 #undef FQ_K
-    set_error("k_pass16: no instantiation for seq=%d ph=%d ma=%d mb=%d", SEQ, ph, ma, mb);
+    set_error("k_pass16: no instantiation for seq=%d ph=%d ma=%d mb=%d k=%d", SEQ, ph, ma, mb, k);
     return FQ_ERR_UNSUPPORTED;
 }
 

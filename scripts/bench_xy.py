@@ -1,6 +1,7 @@
 """XY-mixer layer timing (BASELINE config 4: portfolio n=26, Hamming weight
 13, float64 costs): device time per layer of the tiled XY program, evolved in
-place on a resident state (no initial-state copy), complex128 and complex64."""
+place on a resident state (no initial-state copy), complex128 and complex64,
+and complex128 with gamma = 0 (no phase: the phase share of a layer)."""
 import json
 import os
 import sys
@@ -25,10 +26,10 @@ g, b = rng.uniform(0, 1, p), rng.uniform(0, 1, p)
 for kind in ("xy-ring", "xy-complete"):
     if only and only != kind:
         continue
-    for dt in (torch.complex128, torch.complex64):
+    for dt, gam in ((torch.complex128, g), (torch.complex64, g), (torch.complex128, 0 * g)):
         state = init.to(dt).clone()
         e = torch.empty(1, dtype=torch.float64, device="cuda")
-        layers = [(float(x), float(y), 1, 0, n) for x, y in zip(g, b)]
+        layers = [(float(x), float(y), 1, 0, n) for x, y in zip(gam, b)]
         fn = lambda: run_program(state, n, kind, layers, dc=dc, expectation_out=e)  # noqa: E731
         fn()
         torch.cuda.synchronize()
@@ -41,6 +42,7 @@ for kind in ("xy-ring", "xy-complete"):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         print(json.dumps({"mixer": kind, "dtype": str(dt).split(".")[-1], "n": n, "p": p,
+                          "phase": bool(np.any(gam)),
                           "ms_per_layer": ms / p, "ms_program": ms,
                           "norm": float(torch.linalg.vector_norm(state).item())}), flush=True)
         del state

@@ -162,3 +162,55 @@ def test_large_n_sharded_equals_single_state(n, dtype, Ks, p):
         del dres
         gc.collect()
         torch.cuda.empty_cache()
+
+
+def _last_pass_kinds():
+    """(round program, targets) of every pass of the last X program (fq_last_passes)."""
+    import ctypes
+
+    info = (ctypes.c_int * (5 * 64))()
+    cnt = _lib.load().fq_last_passes(info, None, 64)
+    return [(info[5 * i], info[5 * i + 2]) for i in range(cnt)]
+
+
+@pytest.fixture
+def reset_lane():
+    yield
+    _lib.call("fq_set_option", b"lane3", 1)
+    _lib.call("fq_set_option", b"plan", -1)
+    _lib.call("fq_set_option", b"plan_tmax", 0)
+
+
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+@pytest.mark.parametrize("style", [0, 1])
+def test_lane_butterfly_programs_vs_oracle(dtype, style, reset_lane):
+    """9-target high groups (3 low spectators, tile bit 3 a target: the n = 30
+    config-3 shape) run the two-pattern round programs with tile bit 3 as warp-
+    shuffle butterflies (K_LANE3), light and fused; both RX forms (|tan b| <= 1 and
+    > 1), a gamma = 0 layer (two layers in one light pass) -- against the oracle, and
+    against the same plan with lane3 off (the 8|0|4 programs)."""
+    n, p = 21, 4
+    rng = np.random.default_rng(7 + style)
+    g = rng.uniform(-1, 1, p)
+    g[2] = 0.0
+    b = np.array([0.3, 1.3, -0.4, 1.45])
+    sim = QaoaSimulator(terms=labs_terms(n), dtype=dtype)
+    costs = sim.get_cost_diagonal()
+    ref = O.simulate(costs, g, b)
+    e_ref = O.expectation(ref, costs)
+    tol = ATOL if dtype == "complex128" else 1e-4
+    _lib.call("fq_set_option", b"plan", style)
+    _lib.call("fq_set_option", b"plan_tmax", 9)
+    states = {}
+    for lane in (1, 0):
+        _lib.call("fq_set_option", b"lane3", lane)
+        res = sim.simulate_qaoa(g, b)
+        kinds = _last_pass_kinds()
+        nine = [sq for sq, t in kinds if t == 9]
+        assert nine, kinds
+        # SEQ_84 = 1, SEQ_848 = 3 (two patterns) with lane butterflies; 8|0|4 programs without
+        assert all((sq in (1, 3)) == bool(lane) for sq in nine), (lane, kinds)
+        np.testing.assert_allclose(res.state, ref, rtol=0, atol=tol * np.abs(ref).max(), err_msg=f"lane3={lane}")
+        assert sim.get_expectation(res) == pytest.approx(e_ref, rel=tol)
+        states[lane] = res.state
+    np.testing.assert_allclose(states[1], states[0], rtol=0, atol=(1e-12 if dtype == "complex128" else 1e-5))
