@@ -674,6 +674,7 @@ static int target_mask(const Group &g) {
 // among tile bits 0..3 is bit 3 runs the two-pattern programs with bit 3 as a
 // lane butterfly (K_LANE3)
 static int g_lane3 = 1;
+static int g_cost_l2 = -1;  // cost loads at normal L2 priority: -1 when cost runs < 32 B, 0 never, 1 always
 static int lane_bits(const Group &g, bool lane_ok) {
     return lane_ok && g_lane3 && (target_mask(g) & 0xF) == 0x8 ? 0x8 : 0;
 }
@@ -1048,6 +1049,9 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCt
         P.run_bits = 0;
         while (P.run_bits < kTileBits && g.tile_pos[P.run_bits] == P.run_bits) ++P.run_bits;
         P.pf_cost = (ph != 0 || P.expect) ? 1 : 0;
+        // cost runs shorter than a 32-B sector: the rest of the sector is the neighbouring
+        // tile's, read by another CTA moments later -- keep it in L2 (option cost_l2: -1 auto)
+        P.cost_l2 = g_cost_l2 >= 0 ? g_cost_l2 : ((CB << P.run_bits) < 32 ? 1 : 0);
         ma = P.A.mode;
         mb = two ? P.B.mode : 2;
         if (P.expect && ph == 0 && !two && !seq_heavy(sq)) ph = 3;  // preload the expectation's costs
@@ -1538,6 +1542,7 @@ int fq_set_option(const char *name, int value) {
         {"phase_tables", &g_phase_tables, 0, 1},  // uint16 phase via smem tables (else sincos)
         {"plan", &g_plan, -1, 1},           // group plan: -1 cost model, 0 legacy, 1 small fusion groups
         {"plan_tmax", &g_plan_tmax, 0, 12},  // force the high-group chunk size (0: cost model)
+        {"cost_l2", &g_cost_l2, -1, 1},     // cost loads at normal L2 priority (-1: runs < 32 B)
         {"lane3", &g_lane3, 0, 1},          // 9-target high groups: tile bit 3 as lane butterflies (K_LANE3)
         {"res16", &g_res16, 0, 2},          // n <= 12 X / custom: resident kernel variant (2: k_resident8)
         {"sweep", &g_sweep, 0, 1},          // L2-resident slab sweeps of pass pairs

@@ -80,6 +80,7 @@ struct PassParams {
     int pf_dist;              // L2 prefetch distance in grid strides (0: off)
     int run_bits;             // tile bits 0..run_bits-1 sit at physical bits 0..run_bits-1 (contiguous runs)
     int pf_cost;              // also prefetch the cost slice of the tile
+    int cost_l2;              // cost loads at normal L2 priority (short cost runs), else evict-first
     int lane;                 // K_LANE3 programs: tile bits 0..3 (here only bit 3) that are targets, applied as
                               // lane butterflies (warp shuffles) in the PAT4 rounds
     int sm_rank, sm_shift[5], sm_bits[5];  // state tensor map: rank, outer-dim coordinate = (t >> shift) & (2^bits - 1)
@@ -260,10 +261,18 @@ __device__ __forceinline__ CostRaw<COST> load_cost(const PassParams &P, long lon
     else return (unsigned)__ldcs(static_cast<const unsigned short *>(P.costs) + k);
 }
 
+// l2: keep the line in L2 at normal priority instead of evict-first.  With
+// short cost runs (< 32 B: 3 low spectators x uint16) a sector holds entries of
+// the neighbouring tile, which another CTA reads moments later.
 template <int COST>
-__device__ __forceinline__ CostRaw<COST> load_cost_at(const char *p) {
-    if constexpr (COST == FQ_COST_F64) return __ldcs(reinterpret_cast<const double *>(p));
-    else return (unsigned)__ldcs(reinterpret_cast<const unsigned short *>(p));
+__device__ __forceinline__ CostRaw<COST> load_cost_at(const char *p, int l2 = 0) {
+    if constexpr (COST == FQ_COST_F64) {
+        const double *q = reinterpret_cast<const double *>(p);
+        return l2 ? __ldcg(q) : __ldcs(q);
+    } else {
+        const unsigned short *q = reinterpret_cast<const unsigned short *>(p);
+        return (unsigned)(l2 ? __ldcg(q) : __ldcs(q));
+    }
 }
 
 template <int COST>
@@ -465,12 +474,12 @@ __device__ __forceinline__ void pass_tile(const PassParams &P, long long base, C
             if (PH == 1) {
                 const char *c8 = cs + thr8 * CB;
     #pragma unroll
-                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c8 + P.coff[PAT8][i]);
+                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c8 + P.coff[PAT8][i], P.cost_l2);
             }
             if (PH == 3) {  // the program's last pass: its expectation costs, in the store pattern
                 const char *cl = cs + thrL * CB + (LAST == PAT8 ? 0 : g4c());
     #pragma unroll
-                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i]);
+                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i], P.cost_l2);
             }
             if (PH == 2) {
                 if (P.probe & 1) {
@@ -479,7 +488,7 @@ __device__ __forceinline__ void pass_tile(const PassParams &P, long long base, C
                 } else {
                     const char *c4 = cs + thr4 * CB + g4c();
     #pragma unroll
-                    for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c4 + P.coff[PAT4][i]);
+                    for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c4 + P.coff[PAT4][i], P.cost_l2);
                 }
             }
             auto phase_all = [&]() {
@@ -539,7 +548,7 @@ __device__ __forceinline__ void pass_tile(const PassParams &P, long long base, C
             if (PH != 3 && P.expect) {  // cost entries of the last pattern (final pass with a phase)
                 const char *cl = cs + thrL * CB + (LAST == PAT8 ? 0 : g4c());
     #pragma unroll
-                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i]);
+                for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i], P.cost_l2);
             }
             char *psl = reinterpret_cast<char *>(static_cast<T *>(P.psi) + base + thrL) + (LAST == PAT8 ? 0 : g4s());
     #pragma unroll
