@@ -674,6 +674,7 @@ static int target_mask(const Group &g) {
 // among tile bits 0..3 is bit 3 runs the two-pattern programs with bit 3 as a
 // lane butterfly (K_LANE3)
 static int g_lane3 = 1;
+static int g_cost_stage = 1;  // shared cost tile for the phase / expectation read after a transpose
 static int g_cost_l2 = -1;  // cost loads at normal L2 priority: -1 when cost runs < 32 B, 0 never, 1 always
 static int lane_bits(const Group &g, bool lane_ok) {
     return lane_ok && g_lane3 && (target_mask(g) & 0xF) == 0x8 ? 0x8 : 0;
@@ -1055,6 +1056,18 @@ static int run_x_program(const fq_evolve_desc *d, cudaStream_t st, const ShardCt
         ma = P.A.mode;
         mb = two ? P.B.mode : 2;
         if (P.expect && ph == 0 && !two && !seq_heavy(sq)) ph = 3;  // preload the expectation's costs
+        // uint16 costs read after the first transpose (mid-layer phase, expectation): staged
+        // through a shared cost tile with two 16-B loads per thread, if the tile's runs hold
+        // >= 8 entries and the extra 8.5 KB keeps two CTAs per SM
+        P.cost_stage = 0;
+        if (g_cost_stage && d->cost_kind == FQ_COST_U16 && !global && P.run_bits >= 3 && (ph == 2 || ph == 3)) {
+            const size_t need = (size_t)elem * kTilePadded + (size_t)(kTableLo + table_hi) * 128 +
+                                kCostTileSlots * sizeof(unsigned short);
+            if (need <= 113 * 1024) {
+                P.cost_stage = 1;
+                P.c11 = 2LL << g.tile_pos[kTileBits - 1];
+            }
+        }
     };
     // Passes si and si+1 as one L2-resident slab sweep (sweep.cuh) when the
     // pair has an instantiation and its slab fits the L2 budget; `swept` tells.
@@ -1542,7 +1555,8 @@ int fq_set_option(const char *name, int value) {
         {"phase_tables", &g_phase_tables, 0, 1},  // uint16 phase via smem tables (else sincos)
         {"plan", &g_plan, -1, 1},           // group plan: -1 cost model, 0 legacy, 1 small fusion groups
         {"plan_tmax", &g_plan_tmax, 0, 12},  // force the high-group chunk size (0: cost model)
-        {"cost_l2", &g_cost_l2, -1, 1},     // cost loads at normal L2 priority (-1: runs < 32 B)
+        {"cost_l2", &g_cost_l2, -1, 1},
+        {"cost_stage", &g_cost_stage, 0, 1},  // uint16 costs through a shared cost tile (16-B loads)     // cost loads at normal L2 priority (-1: runs < 32 B)
         {"lane3", &g_lane3, 0, 1},          // 9-target high groups: tile bit 3 as lane butterflies (K_LANE3)
         {"res16", &g_res16, 0, 2},          // n <= 12 X / custom: resident kernel variant (2: k_resident8)
         {"sweep", &g_sweep, 0, 1},          // L2-resident slab sweeps of pass pairs

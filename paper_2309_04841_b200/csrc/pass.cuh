@@ -81,6 +81,9 @@ struct PassParams {
     int run_bits;             // tile bits 0..run_bits-1 sit at physical bits 0..run_bits-1 (contiguous runs)
     int pf_cost;              // also prefetch the cost slice of the tile
     int cost_l2;              // cost loads at normal L2 priority (short cost runs), else evict-first
+    int cost_stage;           // uint16 costs consumed after a transpose: two 16-B loads per thread into a
+                              // shared cost tile instead of 16 scattered 2-B loads (needs run_bits >= 3)
+    long long c11;            // byte offset of tile bit 11 in the uint16 cost vector
     int lane;                 // K_LANE3 programs: tile bits 0..3 (here only bit 3) that are targets, applied as
                               // lane butterflies (warp shuffles) in the PAT4 rounds
     int sm_rank, sm_shift[5], sm_bits[5];  // state tensor map: rank, outer-dim coordinate = (t >> shift) & (2^bits - 1)
@@ -149,12 +152,19 @@ __device__ __forceinline__ long long thread_offset(const PassParams &P, int tid)
     return off;
 }
 
-template <int FROM, int TO, typename T>
-__device__ __forceinline__ void transpose(T *sm, T (&v)[kRegs], int tid) {
+struct NoOp {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+// `mid` runs between the two barriers (shared data written before the first is
+// visible, and every thread is done with it before anyone passes the second).
+template <int FROM, int TO, typename T, typename F = NoOp>
+__device__ __forceinline__ void transpose(T *sm, T (&v)[kRegs], int tid, F mid = F()) {
     T *p = sm + pat_base<FROM>(tid);
 #pragma unroll
     for (int i = 0; i < kRegs; ++i) p[pat_step<FROM>(i)] = v[i];
     __syncthreads();
+    mid();
     const T *q = sm + pat_base<TO>(tid);
 #pragma unroll
     for (int i = 0; i < kRegs; ++i) v[i] = q[pat_step<TO>(i)];
@@ -440,12 +450,33 @@ __device__ __forceinline__ unsigned long long l2_evict_last_policy() {
 // phase / expectation, store.  `base`: the tile's physical base index.
 // Shared by k_pass16 (one tile after another, streaming) and k_sweep (two
 // sub-passes per L2-resident slab).
+// Shared cost tile (uint16 costs, cost_stage): tile index e at slot
+// e + 16 (e >> 8): the 16-B vector writes are conflict-free and so are the
+// 2-B reads of every register pattern (PAT4's lane bit 4 lands 8 banks over).
+template <int PAT>
+__device__ __forceinline__ int cslot_base(int tid) {
+    if (PAT == PAT8) return tid + 16 * (tid >> 8);
+    if (PAT == PAT4) return (tid & 15) + 272 * (tid >> 4);
+    return 16 * tid + 16 * (tid >> 4);  // PAT0: e = 16 tid + i
+}
+template <int PAT>
+__host__ __device__ constexpr int cslot_step(int i) {
+    return PAT == PAT8 ? 272 * i : (PAT == PAT4 ? 16 * i : i);
+}
+constexpr int kCostTileSlots = kTile + kTile / 16;
+
 template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R, bool G, int LD, int ST>
 __device__ __forceinline__ void pass_tile(const PassParams &P, long long base, C2<R> *tile, const C2<R> *tlo,
                                           const C2<R> *thi, long long thr8, long long thr4, double &eacc,
-                                          unsigned long long pol) {
+                                          unsigned long long pol, unsigned short *ctile = nullptr,
+                                          long long thrc = 0) {
     using T = C2<R>;
     const int tid = threadIdx.x;
+    // staged costs: the phase (PH 2) or expectation (PH 3) reads them after the first
+    // transpose, whose barrier orders the cost tile's writes before its reads
+    constexpr bool CST_OK = COST == FQ_COST_U16 && !G && (PH == 2 || PH == 3);
+    const bool cst = CST_OK && ctile != nullptr;
+    uint4 cv0 = make_uint4(0, 0, 0, 0), cv1 = cv0;
     constexpr bool HAS_B = MB != 2;
     constexpr int NR = seq_rounds(SEQ);
     constexpr int LAST = seq_pat(SEQ, NR - 1);
@@ -471,17 +502,47 @@ __device__ __forceinline__ void pass_tile(const PassParams &P, long long base, C
     #pragma unroll
                 for (int i = 0; i < kRegs; ++i) v[i] = tile_load<LD>(reinterpret_cast<const T *>(ps8 + P.roff[PAT8][i]));
             }
+            if constexpr (CST_OK) {
+                if (cst) {  // tile indices 8 tid .. 8 tid + 7 and the same + 2048 (tile bit 11)
+                    const uint4 *c0 = reinterpret_cast<const uint4 *>(cs + thrc * CB);
+                    const uint4 *c1 = reinterpret_cast<const uint4 *>(cs + thrc * CB + P.c11);
+                    cv0 = P.cost_l2 ? __ldcg(c0) : __ldcs(c0);
+                    cv1 = P.cost_l2 ? __ldcg(c1) : __ldcs(c1);
+                }
+            }
+            auto stage_costs = [&]() {  // before the first transpose (its barrier publishes them)
+                if constexpr (CST_OK) {
+                    if (cst) {
+                        uint4 *ct = reinterpret_cast<uint4 *>(ctile);
+                        ct[tid + 2 * (tid >> 5)] = cv0;
+                        ct[tid + 256 + 2 * ((tid + 256) >> 5)] = cv1;
+                    }
+                }
+            };
+            auto read_costs = [&](auto pat) {  // cost entries of pattern PAT from the shared cost tile
+                constexpr int PT = decltype(pat)::value;
+                const unsigned short *c = ctile + cslot_base<PT>(tid);
+    #pragma unroll
+                for (int i = 0; i < kRegs; ++i) raw[i] = (CostRaw<COST>)c[cslot_step<PT>(i)];
+            };
+            // the expectation's costs (store pattern) are read inside the program's LAST
+            // transpose: after it no barrier precedes the next tile's stage_costs
+            auto exp_mid = [&]() {
+                if constexpr (CST_OK) {
+                    if (cst && (PH == 3 || P.expect)) read_costs(std::integral_constant<int, LAST>());
+                }
+            };
             if (PH == 1) {
                 const char *c8 = cs + thr8 * CB;
     #pragma unroll
                 for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(c8 + P.coff[PAT8][i], P.cost_l2);
             }
-            if (PH == 3) {  // the program's last pass: its expectation costs, in the store pattern
+            if (PH == 3 && !cst) {  // the program's last pass: its expectation costs, in the store pattern
                 const char *cl = cs + thrL * CB + (LAST == PAT8 ? 0 : g4c());
     #pragma unroll
                 for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i], P.cost_l2);
             }
-            if (PH == 2) {
+            if (PH == 2 && !cst) {
                 if (P.probe & 1) {
     #pragma unroll
                     for (int i = 0; i < kRegs; ++i) raw[i] = (CostRaw<COST>)((tid * 7 + i * 131) & 1023);
@@ -495,6 +556,9 @@ __device__ __forceinline__ void pass_tile(const PassParams &P, long long base, C
                 // keep the table lookups behind the preceding butterflies: hoisted
                 // early they would hold 64 registers of phase factors and spill
                 asm volatile("" ::: "memory");
+                if constexpr (CST_OK && PH == 2) {
+                    if (cst) read_costs(std::integral_constant<int, PAT4>());
+                }
                 if (P.probe & 4) return;
                 if (P.probe & 2) {
     #pragma unroll
@@ -509,20 +573,23 @@ __device__ __forceinline__ void pass_tile(const PassParams &P, long long base, C
             bfly16<MIX, MA, PAT8, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 0));
             if constexpr (SEQ == SEQ_840) {
                 if (HAS_B) bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 0));
+                stage_costs();
                 transpose<PAT8, PAT0>(tile, v, tid);
                 bfly16<MIX, MA, PAT0, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
                 if (HAS_B) bfly16<MIX, MB, PAT0, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
-                transpose<PAT0, PAT4>(tile, v, tid);
+                transpose<PAT0, PAT4>(tile, v, tid, exp_mid);
                 bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 2));
                 if (HAS_B) bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
             } else if constexpr (SEQ == SEQ_84) {
                 if (HAS_B) bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 0));
-                transpose<PAT8, PAT4>(tile, v, tid);
+                stage_costs();
+                transpose<PAT8, PAT4>(tile, v, tid, exp_mid);
                 bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
                 if constexpr (K == K_LANE3) lane_bfly16<MA, 8, R>(v, P.A);
                 if (HAS_B) bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
                 if constexpr (K == K_LANE3 && HAS_B) lane_bfly16<MB, 8, R>(v, P.B);
             } else if constexpr (SEQ == SEQ_84048) {
+                stage_costs();
                 transpose<PAT8, PAT0>(tile, v, tid);
                 bfly16<MIX, MA, PAT0, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
                 transpose<PAT0, PAT4>(tile, v, tid);
@@ -531,21 +598,22 @@ __device__ __forceinline__ void pass_tile(const PassParams &P, long long base, C
                 bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
                 transpose<PAT4, PAT0>(tile, v, tid);
                 bfly16<MIX, MB, PAT0, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 3));
-                transpose<PAT0, PAT8>(tile, v, tid);
+                transpose<PAT0, PAT8>(tile, v, tid, exp_mid);
                 bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 4));
             } else {  // SEQ_848
+                stage_costs();
                 transpose<PAT8, PAT4>(tile, v, tid);
                 bfly16<MIX, MA, PAT4, R>(v, P.A, round_mask<K, SEQ>(P.maskA, 1));
                 if constexpr (K == K_LANE3) lane_bfly16<MA, 8, R>(v, P.A);
                 phase_all();
                 if constexpr (K == K_LANE3) lane_bfly16<MB, 8, R>(v, P.B);
                 bfly16<MIX, MB, PAT4, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 1));
-                transpose<PAT4, PAT8>(tile, v, tid);
+                transpose<PAT4, PAT8>(tile, v, tid, exp_mid);
                 bfly16<MIX, MB, PAT8, R>(v, P.B, round_mask<K, SEQ>(P.maskB, 2));
             }
             // ---- store (+ expectation) in the last round's pattern
             const R fs = (R)P.final_scale;
-            if (PH != 3 && P.expect) {  // cost entries of the last pattern (final pass with a phase)
+            if (PH != 3 && P.expect && !cst) {  // cost entries of the last pattern (final pass with a phase)
                 const char *cl = cs + thrL * CB + (LAST == PAT8 ? 0 : g4c());
     #pragma unroll
                 for (int i = 0; i < kRegs; ++i) raw[i] = load_cost_at<COST>(cl + P.coff[LAST][i], P.cost_l2);
@@ -600,6 +668,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
     const long long thr8 = thread_offset<PAT8, G>(P, tid);
     const long long thr4 = thread_offset<PAT4, G>(P, tid);
     double eacc = 0.0;
+    // staged costs: thread tid loads tile indices 8 tid .. 8 tid + 7 (tile bits 3..10 = tid bits)
+    unsigned short *ctile = nullptr;
+    long long thrc = 0;
+    if (!G && COST == FQ_COST_U16 && P.cost_stage) {
+        ctile = reinterpret_cast<unsigned short *>(thi + P.table_hi * table_copies<R>());
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if ((tid >> j) & 1) thrc += 1LL << P.tile_pos[3 + j];
+    }
 
     const bool pf = P.pf_dist > 0 && tid == 0;
     if (pf) {  // prologue: tiles 1 .. pf_dist-1 of this CTA
@@ -617,7 +694,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_pass16(const __grid_constant__ 
             const long long tp = t + (long long)P.pf_dist * gridDim.x;
             if (tp < P.n_tiles) prefetch_tile(P, &tm_state, &tm_cost, P.reverse ? P.n_tiles - 1 - tp : tp, !P.init);
         }
-        pass_tile<MIX, COST, SEQ, PH, MA, MB, K, R, G, LD_STREAM, ST_STREAM>(P, base, tile, tlo, thi, thr8, thr4, eacc, 0ull);
+        pass_tile<MIX, COST, SEQ, PH, MA, MB, K, R, G, LD_STREAM, ST_STREAM>(P, base, tile, tlo, thi, thr8, thr4, eacc, 0ull,
+                                                                             ctile, thrc);
     }
     if (P.expect) {
         const double s = block_sum<kThreads>(eacc, red);
@@ -646,13 +724,15 @@ template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R 
 static int launch_pass16(const PassParams &P, const PassMaps &M, int grid, cudaStream_t st) {
     static bool configured = false;
     constexpr int CP = table_copies<R>();
-    const size_t smem = (size_t)(kTilePadded + (kTableLo + kMaxTableHi) * CP) * sizeof(C2<R>);
+    const size_t smem = (size_t)(kTilePadded + (kTableLo + kMaxTableHi) * CP) * sizeof(C2<R>) +
+                        kCostTileSlots * sizeof(unsigned short);
     if (!configured) {
         cudaFuncSetAttribute(k_pass16<MIX, COST, SEQ, PH, MA, MB, K, R, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         configured = true;
     }
-    const size_t need = (size_t)(kTilePadded + (kTableLo + P.table_hi) * CP) * sizeof(C2<R>);
+    const size_t need = (size_t)(kTilePadded + (kTableLo + P.table_hi) * CP) * sizeof(C2<R>) +
+                        (P.cost_stage ? kCostTileSlots * sizeof(unsigned short) : 0);
     k_pass16<MIX, COST, SEQ, PH, MA, MB, K, R, G><<<grid, kThreads, need, st>>>(P, M.state, M.cost);
     FQ_LAUNCHED("k_pass16");
     return FQ_OK;
