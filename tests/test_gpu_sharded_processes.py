@@ -3,7 +3,8 @@ processes on one B200 (the round's boxes have one GPU): gloo carries the
 exchange through host memory, everything else is the production code —
 shard-local precompute by index offset, fused local passes, Alg. 4 exchange
 order, all-reduced observables.  Compared against the single-GPU simulator
-and the oracle.  (On an 8-GPU node the same code runs over NCCL.)"""
+and directly against the CPU oracle.  (On an 8-GPU node the same code runs
+over NCCL.)"""
 
 import os
 import socket
@@ -109,8 +110,19 @@ def _run_processes(world, n, p, kind, chunk, mode, dev_barrier, dtype=None):
     full = np.concatenate([o[4] for o in out])
     tol = 1e-12 if dtype is None else 1e-4 * np.abs(res.state).max()  # complex64: the fp32 tolerance
     np.testing.assert_allclose(full, res.state, rtol=0, atol=tol)
+    # and directly against the CPU oracle (not only CUDA against CUDA)
+    costs = sim.get_cost_diagonal()
+    factory = None
+    if kind == "custom":
+        mixer = _mixer(kind, n)
+        factory = lambda beta: [(u.a, u.b) for u in mixer.su2_factory(beta)]  # noqa: E731
+    ref = O.simulate(costs, g, b, kind, init, su2_factory=factory)
+    otol = 1e-10 if dtype is None else 1e-4
+    np.testing.assert_allclose(full, ref, rtol=0, atol=otol * np.abs(ref).max())
+    e_ref = O.expectation(ref, costs)
     for rank, E, ov, ex, _ in out:
         assert E == pytest.approx(sim.get_expectation(res), rel=1e-10 if dtype is None else 1e-4, abs=1e-12)
+        assert E == pytest.approx(e_ref, rel=otol, abs=1e-12)
         assert ov == pytest.approx(sim.get_overlap(res), abs=1e-12 if dtype is None else 1e-4)
         if kind in ("x", "custom"):
             assert ex == 2 * p  # Alg. 4: two exchanges per layer
