@@ -267,6 +267,116 @@ def run_config3(args):
         return {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
 
+def run_config1():
+    """BASELINE config 1: LABS n=12 p=4 (the reference's CPU-runnable case): device
+    time of one evaluation back to back (the one-CTA resident kernel) and the
+    batched throughput (4096 parameter sets, one CTA each)."""
+    import torch
+
+    from paper_2309_04841_b200 import QaoaSimulator, labs_terms
+
+    try:
+        n, p = 12, 4
+        g, b = angles(p)
+        sim = QaoaSimulator(terms=labs_terms(n))
+        rng = np.random.default_rng(1)
+        B = 4096
+        G, Bt = rng.uniform(0, 1, (B, p)), rng.uniform(0, 1, (B, p))
+        for _ in range(50):
+            sim.simulate_qaoa_batched(G, Bt)
+        ms1 = _event_ms(lambda: sim.simulate_qaoa(g, b, reuse_buffer=True), 200, 1)
+        msb = _event_ms(lambda: sim.simulate_qaoa_batched(G, Bt), 10, 1)
+        t0 = time.perf_counter()
+        for _ in range(200):
+            sim.objective(g, b)
+        call_ms = (time.perf_counter() - t0) / 200 * 1e3
+        out = {"workload": "LABS n=12 p=4 X-mixer complex128", "device_us_per_eval": ms1 * 1e3,
+               "objective_call_us": call_ms * 1e3, "batched_evals_per_s": B / (msb / 1e3), "batch": B}
+        del sim
+        torch.cuda.empty_cache()
+        return out
+    except Exception as exc:  # noqa: BLE001 - an extra key never fails the headline line
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
+
+def run_config2():
+    """BASELINE config 2: MaxCut random 3-regular n=26 p=6 (the committed graph
+    tests/golden/maxcut26.edges), evals/s and the HBM roofline of the step."""
+    import torch
+
+    from paper_2309_04841_b200 import Graph, QaoaSimulator, _lib, maxcut_terms
+    from paper_2309_04841_b200.mixers import run_program
+
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "maxcut26.edges")) as f:
+            edges = [tuple(int(x) for x in ln.split()) for ln in f if ln.strip() and not ln.startswith("#")]
+        n, p = 26, 6
+        g, b = angles(p)
+        sim = QaoaSimulator(terms=maxcut_terms(Graph.from_edges(n, edges)))
+        dc = sim.device_costs
+        state = torch.empty(1 << n, dtype=torch.complex128, device="cuda")
+        e = torch.empty(1, dtype=torch.float64, device="cuda")
+        layers = [(float(x), float(y), 1, 0, n) for x, y in zip(g, b)]
+        fn = lambda: run_program(state, n, "x", layers, dc=dc, init=True,  # noqa: E731
+                                 init_amp=1 / math.sqrt(1 << n), expectation_out=e)
+        for _ in range(3):
+            fn()
+        ms = _event_ms(fn, 20, 1)
+        lay = (_lib.FqLayer * p)(*[_lib.FqLayer(*t) for t in layers])
+        passes = _lib.load().fq_plan_x_passes(n, p, lay, 0)
+        S, C = 16 << n, dc.nbytes_per_amp() << n
+        byts = passes * 2 * S - S + (p + 1) * C
+        peak, _ = load_peaks()
+        out = {"workload": "MaxCut 3-regular n=26 p=6 X-mixer complex128 objective", "ms_per_eval": ms,
+               "evals_per_s": 1e3 / ms, "passes_per_eval": passes, "hbm_bytes_per_eval": byts,
+               "roofline_frac_hbm": byts / (ms / 1e3) / 1e9 / peak, "objective": float(e.item()),
+               "cost_encoding": "uint16" if dc.u16 is not None else "float64"}
+        del sim, dc, state
+        torch.cuda.empty_cache()
+        return out
+    except Exception as exc:  # noqa: BLE001
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
+
+def run_config4():
+    """BASELINE config 4: portfolio n=26 (float64 costs) under the XY-ring and
+    XY-complete mixers from the Hamming-weight-13 state: device ms per layer
+    (p = 4 in place, phase + mixer) and the HBM roofline of the tiled XY passes."""
+    import torch
+
+    from paper_2309_04841_b200 import QaoaSimulator, _lib, hamming_weight_state
+    from paper_2309_04841_b200.mixers import run_program
+    from paper_2309_04841_b200.problems import portfolio_terms
+
+    try:
+        n, p = 26, 4
+        g, b = angles(p)
+        sim = QaoaSimulator(terms=portfolio_terms(n))
+        dc = sim.device_costs
+        init = torch.from_numpy(hamming_weight_state(n, n // 2)).cuda()
+        peak, _ = load_peaks()
+        out = {"workload": "portfolio n=26 (float64 costs), Hamming weight 13, p=4 in place"}
+        for kind in ("xy-ring", "xy-complete"):
+            state = init.clone()
+            e = torch.empty(1, dtype=torch.float64, device="cuda")
+            layers = [(float(x), float(y), 1, 0, n) for x, y in zip(g, b)]
+            fn = lambda: run_program(state, n, kind, layers, dc=dc, expectation_out=e)  # noqa: E731
+            fn()
+            ms = _event_ms(fn, 3, 1) / p
+            rounds = ctypes.c_int()
+            passes = _lib.load().fq_plan_xy_passes(n, _lib.MIXER_CODES[kind], ctypes.byref(rounds))
+            S, C = 16 << n, dc.nbytes_per_amp() << n
+            byts = passes * 2 * S + C  # per layer: every pass reads + writes the state, the phase reads the costs
+            out[kind] = {"ms_per_layer": ms, "passes_per_layer": passes, "register_rounds_per_layer": rounds.value,
+                         "hbm_bytes_per_layer": byts, "roofline_frac_hbm": byts / (ms / 1e3) / 1e9 / peak}
+            del state
+        del sim, dc, init
+        torch.cuda.empty_cache()
+        return out
+    except Exception as exc:  # noqa: BLE001
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
+
 def run_config5(args, world, rank, k, barrier):
     """BASELINE config 5 / north star: LABS n=34 p=10 complex128 sharded over the
     N ranks (fused sharded program: local passes on each shard, global-group
@@ -665,7 +775,10 @@ def main():
         del sim, dc
         torch.cuda.empty_cache()
         if world == 1:
+            extra["config1"] = run_config1()
+            extra["config2"] = run_config2()
             extra["config3"] = run_config3(args)
+            extra["config4"] = run_config4()
         extra["config5"] = run_config5(args, world, rank, k, barrier)
     if rank == 0:
         line = {

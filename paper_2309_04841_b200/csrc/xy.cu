@@ -14,6 +14,8 @@
 // complete layer at n = 26); here a handful of passes per layer.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -777,6 +779,20 @@ int run_xy_tiled(const fq_evolve_desc *d, const std::vector<std::pair<int, int>>
 
 int plan_xy_passes(int n, int mixer, const std::vector<std::pair<int, int>> &gates, int *rounds) {
     const auto plans = plan_xy(n, gates, mixer);
+    if (std::getenv("FQ_XY_DUMP")) {  // development: the plan on stderr (tile qubits; per round: register tile bits / gates)
+        for (auto &pl : plans) {
+            std::fprintf(stderr, "pass tile=");
+            for (int q : pl.tile) std::fprintf(stderr, "%d,", q);
+            std::fprintf(stderr, "\n");
+            for (size_t r = 0; r < pl.round_bits.size(); ++r) {
+                std::fprintf(stderr, "  R");
+                for (int b : pl.round_bits[r]) std::fprintf(stderr, " %d", b);
+                std::fprintf(stderr, " :");
+                for (auto &g : pl.round_gates[r]) std::fprintf(stderr, " (%d,%d)", g.first, g.second);
+                std::fprintf(stderr, "\n");
+            }
+        }
+    }
     if (rounds) {
         *rounds = 0;
         for (auto &pl : plans) *rounds += (int)pl.round_bits.size();
