@@ -325,13 +325,22 @@ int fq_plan_xy_passes(int n, int mixer, int *rounds);
  * arrays are skipped. */
 int fq_last_passes(int *info, float *ms, int max);
 
-/* Runtime switches (testing / A-B measurement):
- *   "prefetch"     L2 bulk-prefetch distance of the pass kernel in grid strides (default 1, 0 = off)
+/* Runtime switches (testing / A-B measurement; Python: FQ_OPTIONS="name=value,..."
+ * applies them when the library is loaded).  The main ones:
+ *   "prefetch"     L2 tensor-prefetch distance of the pass kernel in grid strides
+ *                  (default -1: 1 for runs >= 256 B, else 0)
  *   "fuse"         fuse the passes at layer boundaries (default 1)
  *   "phase_tables" uint16 phase through shared-memory tables (default 1, 0 = sincos)
  *   "plan"         group plan: -1 cost model (default), 0 legacy, 1 small fusion groups
+ *   "plan_tmax"    force the high-group chunk size (0 = cost model; plan-shape tests)
+ *   "lane3"        9-target high groups as two-pattern programs with tile bit 3 as
+ *                  warp-shuffle butterflies (default 1)
+ *   "cost_l2"      cost loads at normal L2 priority (-1 = when cost runs < 32 B, default)
+ *   "cost_stage"   uint16 costs of the mid-layer phase / expectation through a shared
+ *                  cost tile (default 1)
  *   "time_passes"  record a CUDA event after every pass (read with fq_last_passes)
- *   "xy_tiled"     tiled XY passes (default 1; 0 = one pair kernel per gate) */
+ *   "xy_tiled"     tiled XY passes (default 1; 0 = one pair kernel per gate)
+ * The full list (with ranges) is the table in evolve.cu:fq_set_option. */
 int fq_set_option(const char *name, int value);
 
 #ifdef __cplusplus

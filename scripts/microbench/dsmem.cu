@@ -56,6 +56,31 @@ __global__ void __launch_bounds__(kThreads, 2) k_local(int iters, double *sink) 
     if (s == 12345.678) sink[blockIdx.x] = s;
 }
 
+// 1-bit register <-> lane swap through warp shuffles (an XY round change of one
+// register bit to a lane bit): 8 of 16 registers cross to lane ^ 1
+__global__ void __launch_bounds__(kThreads, 2) k_shfl_swap(int iters, double *sink) {
+    const int tid = threadIdx.x;
+    const bool hi = tid & 1;
+    double2 v[kRegs];
+#pragma unroll
+    for (int i = 0; i < kRegs; ++i) v[i] = make_double2(tid + i, blockIdx.x);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < kRegs / 2; ++i) {
+            const double2 send = hi ? v[i] : v[i + kRegs / 2];
+            double2 r;
+            r.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
+            r.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+            if (hi) v[i] = r;
+            else v[i + kRegs / 2] = r;
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < kRegs; ++i) s += v[i].x + v[i].y;
+    if (s == 12345.678) sink[blockIdx.x] = s;
+}
+
 template <int C, bool WRITE>
 __global__ void __launch_bounds__(kThreads, 1) k_dsmem(int iters, double *sink) {
     extern __shared__ double2 sm[];
@@ -150,6 +175,12 @@ int main() {
         printf("{\"variant\": \"local transpose\", \"ctas_per_sm\": %d, \"ns_per_step\": %.1f, "
                "\"smem_B_per_clk_per_sm\": %.1f}\n",
                per_sm, ns, bytes_per_sm / (ns * 1e-9 * clk_khz * 1e3));
+    }
+    for (int per_sm = 1; per_sm <= 2; ++per_sm) {
+        const float ms = time_kernel(k_shfl_swap, dim3(per_sm * sms), 0, iters, sink, 1);
+        const double ns = ms * 1e6 / iters;
+        printf("{\"variant\": \"shuffle 1-bit swap (8 of 16 registers)\", \"ctas_per_sm\": %d, "
+               "\"ns_per_step\": %.1f}\n", per_sm, ns);
     }
     auto run = [&](auto kern, int C, const char *name) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -19,7 +19,7 @@ from paper_2309_04841_b200.distributed import simulate_qaoa_distributed  # noqa:
 
 def one(seed):
     rng = np.random.default_rng(seed)
-    n = int(rng.integers(13, 21))
+    n = int(rng.integers(13, 23))  # n = 21: 12 + 9-target groups (lane butterflies)
     p = int(rng.integers(0, 5))
     kind = ["x", "x", "custom", "xy-ring", "xy-complete"][int(rng.integers(0, 5))]
     if kind == "xy-complete":
