@@ -261,3 +261,40 @@ def test_planner_shapes_host_only():
     # sharded register (k global qubits): the global qubits share one group
     d = _lib.describe_x_plan(34, 4, k=3)
     assert any({"31", "32", "33"} <= set(g.split("/")[0].split(",")) for g in d.split(" ")[0][7:].split(";"))
+
+
+def test_round2_options_and_n30_plan_host_only():
+    """Run-time options of this round's kernel paths are accepted with their ranges
+    (lane butterflies, cost L2 policy, shared cost tile) and rejected outside them;
+    LABS n = 30 plans three groups with 9-target high groups (the lane-butterfly
+    shape, K_LANE3) and 21 passes for p = 10."""
+    from paper_2309_04841_b200 import _lib
+
+    for name, good, bad in ((b"lane3", (0, 1), 2), (b"cost_l2", (-1, 0, 1), 2), (b"cost_stage", (0, 1), -1)):
+        for v in good:
+            _lib.call("fq_set_option", name, v)
+        with pytest.raises(ValueError):
+            _lib.call("fq_set_option", name, bad)
+    _lib.call("fq_set_option", b"lane3", 1)
+    _lib.call("fq_set_option", b"cost_l2", -1)
+    _lib.call("fq_set_option", b"cost_stage", 1)
+    d30 = _lib.describe_x_plan(30, 10)
+    groups = d30.split(" ")[0][len("groups="):].split(";")
+    assert sorted(len(g.split("/")[0].split(",")) for g in groups) == [9, 9, 12]
+    assert len(d30.split("passes=")[1].split(",")) == 21
+
+
+def test_fq_options_env_applied_at_load():
+    """FQ_OPTIONS="name=value,..." is applied when the library is loaded (A/B runs of
+    the suite under a kernel variant) and a bad entry fails loudly."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = "from paper_2309_04841_b200 import _lib; _lib.load(); print('loaded')"
+    env = dict(os.environ, FQ_OPTIONS="lane3=0,cost_stage=0")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
+    assert out.returncode == 0 and "loaded" in out.stdout, out.stderr
+    env = dict(os.environ, FQ_OPTIONS="no_such_option=1")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
+    assert out.returncode != 0 and "FQ_OPTIONS" in out.stderr
