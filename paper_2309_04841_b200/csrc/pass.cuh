@@ -446,10 +446,6 @@ __device__ __forceinline__ unsigned long long l2_evict_last_policy() {
     return pol;
 }
 
-// One tile of a pass: load (or generate |+>), the round program SEQ with its
-// phase / expectation, store.  `base`: the tile's physical base index.
-// Shared by k_pass16 (one tile after another, streaming) and k_sweep (two
-// sub-passes per L2-resident slab).
 // Shared cost tile (uint16 costs, cost_stage): tile index e at slot
 // e + 16 (e >> 8): the 16-B vector writes are conflict-free and so are the
 // 2-B reads of every register pattern (PAT4's lane bit 4 lands 8 banks over).
@@ -465,6 +461,10 @@ __host__ __device__ constexpr int cslot_step(int i) {
 }
 constexpr int kCostTileSlots = kTile + kTile / 16;
 
+// One tile of a pass: load (or generate |+>), the round program SEQ with its
+// phase / expectation, store.  `base`: the tile's physical base index.
+// Shared by k_pass16 (one tile after another, streaming) and k_sweep (two
+// sub-passes per L2-resident slab).
 template <int MIX, int COST, int SEQ, int PH, int MA, int MB, int K, typename R, bool G, int LD, int ST>
 __device__ __forceinline__ void pass_tile(const PassParams &P, long long base, C2<R> *tile, const C2<R> *tlo,
                                           const C2<R> *thi, long long thr8, long long thr4, double &eacc,
