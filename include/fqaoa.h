@@ -212,6 +212,18 @@ int fq_qaoa_evolve(const fq_evolve_desc *desc, void *stream);
  * ABI crossing per evaluation. */
 int fq_qaoa_objective(const fq_evolve_desc *desc, double *out_host, void *stream);
 
+/* The same evaluation for small states (n <= 12, X mixer from |+>, complex128,
+ * p <= 64) as a captured CUDA graph replayed per call (the optimiser loop of
+ * BASELINE config 1): create() captures the one-CTA resident program once per
+ * descriptor, reading the angles ang_host[2p] = (gamma_l, beta_l) from and
+ * writing the objective to *out_host -- both PINNED host buffers, accessed by
+ * the kernel directly (no copies); run() orders it behind `stream`, launches
+ * the graph and synchronises, after the caller wrote new angles into ang_host.
+ * desc's device buffers (state, costs) must outlive the handle. */
+int fq_objective_graph_create(const fq_evolve_desc *desc, const double *ang_host, double *out_host, void **handle);
+int fq_objective_graph_run(void *handle, void *stream);
+int fq_objective_graph_destroy(void *handle);
+
 /* Batched small-n evolution: `batch` independent parameter sets (gammas/betas
  * host arrays [batch][p]) for the same cost vector, each evolved from |+>^n
  * (or from psi_init if non-NULL, complex128[2^n] device) entirely on chip;

@@ -69,6 +69,9 @@ _SIGS = {
     "fq_rebase_u16": ([P, I64, I, P], I),
     "fq_qaoa_evolve": ([ctypes.POINTER(FqEvolveDesc), P], I),
     "fq_qaoa_objective": ([ctypes.POINTER(FqEvolveDesc), ctypes.POINTER(D), P], I),
+    "fq_objective_graph_create": ([ctypes.POINTER(FqEvolveDesc), P, P, ctypes.POINTER(P)], I),
+    "fq_objective_graph_run": ([P, P], I),
+    "fq_objective_graph_destroy": ([P], I),
     "fq_qaoa_evolve_sharded": ([ctypes.POINTER(FqEvolveDesc), ctypes.POINTER(FqShardDesc), P], I),
     "fq_plan_sharded_passes": ([I, I, I, ctypes.POINTER(FqLayer), P], I),
     "fq_qaoa_evolve_batched": ([I, I, P, I, D, D, I, I, P, P, P, P, P, P], I),
@@ -157,7 +160,15 @@ def device() -> torch.device:
     return dev
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream() -> int:
+    """The caller's current CUDA stream (raw handle).  The direct C++ query costs
+    ~0.3 us against ~3 us for torch.cuda.current_stream(): on the path of every
+    small-n call."""
+    if _raw_stream is not None:
+        return _raw_stream(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
 
 

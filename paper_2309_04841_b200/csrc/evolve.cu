@@ -63,9 +63,21 @@ struct ResParams {
     unsigned char gates[kResMaxGates][2];
     // per (batch row, layer) angles: gam[b*p + l], bet[b*p + l]; row b = blockIdx.x
     double gam[kResMaxLayers], bet[kResMaxLayers];
+    const double *ang;      // non-null (one parameter set): device [2p] = gamma_l, beta_l, read instead of
+                            // gam / bet -- a captured CUDA graph replays with new angles (fq_objective_graph_*)
     unsigned char phase_on[kResMaxLayers];  // indexed by layer (shared by all rows)
     unsigned char qlo[kResMaxLayers], qhi[kResMaxLayers];  // X/custom qubit range per layer
 };
+
+// Graph-replayed objective (ResParams::ang set): the angles live in pinned host
+// memory the device reads directly; staged once per CTA in shared memory.
+constexpr int kResGraphMaxLayers = 64;
+__device__ __forceinline__ void res_stage_angles(const ResParams &P, double *s_ang) {
+    if (P.ang) {
+        for (int i = threadIdx.x; i < 2 * P.p; i += blockDim.x) s_ang[i] = P.ang[i];
+        __syncthreads();
+    }
+}
 
 template <int COST>
 __device__ __forceinline__ double2 res_phase(const void *costs, int k, double gamma, double scale, double offset) {
@@ -82,6 +94,8 @@ __global__ void __launch_bounds__(kResThreads) k_resident(const __grid_constant_
                                                           const double *__restrict__ su2) {
     extern __shared__ double2 st[];
     __shared__ double red[kResThreads / 32];
+    __shared__ double s_ang[2 * kResGraphMaxLayers];
+    res_stage_angles(P, s_ang);
     const int n = P.n, N = 1 << n, tid = threadIdx.x;
     const int b = blockIdx.x;
     if (P.init || P.psi_in == nullptr) {
@@ -92,8 +106,8 @@ __global__ void __launch_bounds__(kResThreads) k_resident(const __grid_constant_
     }
     __syncthreads();
     for (int l = 0; l < P.p; ++l) {
-        const double gamma = P.gam[b * P.p + l];
-        const double beta = P.bet[b * P.p + l];
+        const double gamma = P.ang ? s_ang[2 * l] : P.gam[b * P.p + l];
+        const double beta = P.ang ? s_ang[2 * l + 1] : P.bet[b * P.p + l];
         if (P.phase_on[l] && gamma != 0.0) {
             for (int k = tid; k < N; k += kResThreads)
                 st[k] = cmul(st[k], res_phase<COST>(P.costs, k, gamma, P.cost_scale, P.cost_offset));
@@ -207,6 +221,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_resident16(const __grid_constan
     double2 *tlo = tile + kTilePadded;
     double2 *thi = tlo + kTableLo * 8;
     __shared__ double red[kThreads / 32];
+    __shared__ double s_ang[2 * kResGraphMaxLayers];
+    res_stage_angles(P, s_ang);
     const int tid = threadIdx.x, N = 1 << P.n, b = blockIdx.x;
     const int table_hi = COST == FQ_COST_U16 ? P.table_hi : 0;
     double2 v[kRegs];
@@ -220,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_resident16(const __grid_constan
     int pat = PAT8;
 #pragma unroll 1
     for (int l = 0; l < P.p; ++l) {
-        const double gamma = P.gam[b * P.p + l];
+        const double gamma = P.ang ? s_ang[2 * l] : P.gam[b * P.p + l];
         if (P.phase_on[l] && gamma != 0.0) {
             if (COST == FQ_COST_U16 && table_hi > 0) {
                 // the previous layer's lookups are behind its transposes' barriers
@@ -248,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_resident16(const __grid_constan
         int mode = 0;
         if (MIX == MIX_RX) {
             double s, c;
-            sincos(P.bet[b * P.p + l], &s, &c);
+            sincos(P.ang ? s_ang[2 * l + 1] : P.bet[b * P.p + l], &s, &c);
             if (fabs(c) >= fabs(s)) { rc = s / c; f = c; }
             else { mode = 1; rc = c / s; f = s; }
         }
@@ -348,6 +364,8 @@ __global__ void __launch_bounds__(kRes8Threads, 1) k_resident8(const __grid_cons
     double2 *tlo = tile + kRes8Padded;
     double2 *thi = tlo + kTableLo * 8;
     __shared__ double red[kRes8Threads / 32];
+    __shared__ double s_ang[2 * kResGraphMaxLayers];
+    res_stage_angles(P, s_ang);
     const int tid = threadIdx.x, N = 1 << P.n, b = blockIdx.x;
     const int table_hi = COST == FQ_COST_U16 ? P.table_hi : 0;
     double2 v[kRes8Regs];
@@ -361,7 +379,7 @@ __global__ void __launch_bounds__(kRes8Threads, 1) k_resident8(const __grid_cons
     }
 #pragma unroll 1
     for (int l = 0; l < P.p; ++l) {
-        const double gamma = P.gam[b * P.p + l];
+        const double gamma = P.ang ? s_ang[2 * l] : P.gam[b * P.p + l];
         if (P.phase_on[l] && gamma != 0.0) {
             if (COST == FQ_COST_U16 && table_hi > 0) {
                 build_phase_tables<double>(tlo, thi, table_hi, gamma, P.cost_scale, P.cost_offset);
@@ -386,7 +404,7 @@ __global__ void __launch_bounds__(kRes8Threads, 1) k_resident8(const __grid_cons
         int mode = 0;
         if (MIX == MIX_RX) {
             double sn, cs;
-            sincos(P.bet[b * P.p + l], &sn, &cs);
+            sincos(P.ang ? s_ang[2 * l + 1] : P.bet[b * P.p + l], &sn, &cs);
             if (fabs(cs) >= fabs(sn)) { rc = sn / cs; f = cs; }
             else { mode = 1; rc = cs / sn; f = sn; }
         }
@@ -1457,11 +1475,118 @@ static int run_resident_program(const fq_evolve_desc *d, cudaStream_t st) {
     return FQ_OK;
 }
 
+// One objective evaluation of a small state (n <= 12, X mixer, from |+>) as a
+// captured CUDA graph: H2D copy of the angles from a pinned host array into a
+// device buffer the resident kernel reads (ResParams::ang), the kernel, D2H
+// copy of the objective into a pinned host double.  Replaying it needs one
+// graph launch per evaluation instead of building and launching the program.
+struct ObjGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev = nullptr;
+};
+
+static void obj_graph_free(ObjGraph *g) {
+    if (!g) return;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    if (g->ev) cudaEventDestroy(g->ev);
+    if (g->st) cudaStreamDestroy(g->st);
+    delete g;
+}
+
 }  // namespace fq
 
 using namespace fq;
 
 extern "C" {
+
+int fq_objective_graph_create(const fq_evolve_desc *d, const double *ang_host, double *out_host, void **handle) {
+    FQ_CHECK_ARG(d && ang_host && out_host && handle, "fq_objective_graph_create: null argument");
+    FQ_CHECK_ARG(d->n >= 1 && d->n <= kTileBits && d->mixer == FQ_MIXER_X && d->init && d->expectation_dev &&
+                     d->state_kind == FQ_STATE_C128 && d->n_layers >= 1 && d->n_layers <= kResGraphMaxLayers &&
+                     d->layers && d->psi && d->costs,
+                 "fq_objective_graph_create: n <= %d complex128, X mixer from |+>, 1..%d layers, with an expectation",
+                 kTileBits, kResGraphMaxLayers);
+    FQ_CHECK_ARG(d->cost_kind == FQ_COST_F64 || d->cost_kind == FQ_COST_U16, "fq_objective_graph_create: bad cost kind");
+    *handle = nullptr;
+    ObjGraph *g = new ObjGraph;
+    const int p = d->n_layers;
+    auto fail = [&](cudaError_t e, const char *what) {
+        const int s = cuda_status(e, what);
+        obj_graph_free(g);
+        return s;
+    };
+    // the kernel reads the angles from, and writes the objective to, the pinned host
+    // buffers themselves (their device-side aliases): the graph is the kernel alone
+    double *ang_dev = nullptr, *out_dev = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&ang_dev), const_cast<double *>(ang_host), 0);
+    if (e != cudaSuccess) return fail(e, "cudaHostGetDevicePointer(angles): ang_host must be pinned");
+    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&out_dev), out_host, 0)) != cudaSuccess)
+        return fail(e, "cudaHostGetDevicePointer(objective): out_host must be pinned");
+    if ((e = cudaStreamCreateWithFlags(&g->st, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "cudaStreamCreate");
+    if ((e = cudaEventCreateWithFlags(&g->ev, cudaEventDisableTiming)) != cudaSuccess) return fail(e, "cudaEventCreate");
+    ResParams *P = new ResParams;
+    std::memset(P, 0, sizeof *P);
+    P->n = d->n;
+    P->p = p;
+    P->mixer = d->mixer;
+    P->costs = d->costs;
+    P->cost_scale = d->cost_scale;
+    P->cost_offset = d->cost_offset;
+    P->init = 1;
+    P->init_amp = d->init_amp;
+    P->psi_out = static_cast<double2 *>(d->psi);
+    P->exp_out = out_dev;
+    P->table_hi = d->cost_kind == FQ_COST_U16 && g_phase_tables ? table_rows(d->cost_levels) : 0;
+    P->ang = ang_dev;
+    for (int i = 0; i < p; ++i) {
+        P->phase_on[i] = (unsigned char)(d->layers[i].apply_phase != 0);
+        P->qlo[i] = (unsigned char)std::max(0, std::min(d->n, d->layers[i].q_lo));
+        P->qhi[i] = (unsigned char)std::max((int)P->qlo[i], std::min(d->n, d->layers[i].q_hi));
+    }
+    auto enqueue = [&]() -> int {
+        return d->cost_kind == FQ_COST_U16 ? launch_resident<FQ_COST_U16>(*P, 1, nullptr, g->st)
+                                           : launch_resident<FQ_COST_F64>(*P, 1, nullptr, g->st);
+    };
+    // once eagerly (kernel attributes, module loading; after the device's pending work,
+    // e.g. the diagonal's precompute on the caller's stream), then captured
+    int s = FQ_OK;
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) s = cuda_status(e, "cudaDeviceSynchronize");
+    if (!s) s = enqueue();
+    if (!s && (e = cudaStreamSynchronize(g->st)) != cudaSuccess) s = cuda_status(e, "cudaStreamSynchronize");
+    if (!s && (e = cudaStreamBeginCapture(g->st, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+        s = cuda_status(e, "cudaStreamBeginCapture");
+    if (!s) {
+        const int s2 = enqueue();
+        e = cudaStreamEndCapture(g->st, &g->graph);
+        s = s2 ? s2 : (e != cudaSuccess ? cuda_status(e, "cudaStreamEndCapture") : FQ_OK);
+    }
+    if (!s && (e = cudaGraphInstantiate(&g->exec, g->graph, 0)) != cudaSuccess) s = cuda_status(e, "cudaGraphInstantiate");
+    delete P;
+    if (s) {
+        obj_graph_free(g);
+        return s;
+    }
+    *handle = g;
+    return FQ_OK;
+}
+
+int fq_objective_graph_run(void *handle, void *stream) {
+    FQ_CHECK_ARG(handle, "fq_objective_graph_run: null handle");
+    ObjGraph *g = static_cast<ObjGraph *>(handle);
+    // on the caller's stream (ordered behind its work), then wait for it
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FQ_CUDA(cudaGraphLaunch(g->exec, st));
+    FQ_CUDA(cudaStreamSynchronize(st));
+    return FQ_OK;
+}
+
+int fq_objective_graph_destroy(void *handle) {
+    obj_graph_free(static_cast<ObjGraph *>(handle));
+    return FQ_OK;
+}
 
 int fq_qaoa_evolve(const fq_evolve_desc *d, void *stream) {
     FQ_CHECK_ARG(d && d->psi && d->n >= 1 && d->n <= 40, "fq_qaoa_evolve: bad descriptor");

@@ -10,6 +10,7 @@ accessors return host (CPU) values, as in the paper's API.
 from __future__ import annotations
 
 import ctypes
+import weakref
 from collections import OrderedDict
 from dataclasses import dataclass
 from math import sqrt
@@ -209,6 +210,31 @@ def _evolve(dc: DeviceCosts, n: int, mixer: Mixer, params: QaoaParams, initial,
     return QaoaResult(state, dc, exp_dev)
 
 
+class _ObjectiveGraph:
+    """A captured one-evaluation CUDA graph for n <= 12 (fq_objective_graph_*):
+    pinned angle / objective buffers the kernel reads and writes directly, the
+    graph handle, and references to the device buffers it uses (they must
+    outlive it)."""
+
+    def __init__(self, desc, p: int, state: torch.Tensor, exp_dev: torch.Tensor):
+        self._ang_t = torch.empty(2 * p, dtype=torch.float64, pin_memory=True)
+        self._out_t = torch.zeros(1, dtype=torch.float64, pin_memory=True)
+        self.ang = self._ang_t.numpy()
+        self._out = self._out_t.numpy()
+        self._keep = (desc, state, exp_dev)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().fq_objective_graph_create(ctypes.byref(desc), self._ang_t.data_ptr(),
+                                                         self._out_t.data_ptr(), ctypes.byref(h)),
+                   "fq_objective_graph_create")
+        self._h = h
+        self._finalizer = weakref.finalize(self, _lib.load().fq_objective_graph_destroy, h)
+
+    def run(self) -> float:
+        _lib.check(_lib.load().fq_objective_graph_run(self._h, _lib.stream()), "fq_objective_graph_run")
+        return float(self._out[0])
+
+
+
 class QaoaSimulator:
     """Simulator bound to one problem; the cost diagonal is computed once, on
     the GPU, at construction (reference qaoa.py:106-166)."""
@@ -238,6 +264,7 @@ class QaoaSimulator:
         self.mixer = Mixer.parse(mixer)
         self._buffer: torch.Tensor | None = None
         self._obj_ctx = None  # objective(): prepared descriptor for the last depth
+        self._graph_ctx = None  # objective(), n <= 12: captured CUDA graph for the last depth
 
     @property
     def device_costs(self) -> DeviceCosts:
@@ -261,6 +288,8 @@ class QaoaSimulator:
             out = self._buffer
         return _evolve(self._dc, self.n, self.mixer, params, initial, out=out, dtype=self.dtype)
 
+    use_graph = True  # objective() for n <= 12: replay a captured CUDA graph (fq_objective_graph_*)
+
     def objective(self, gammas: Sequence[float], betas: Sequence[float], initial=None) -> float:
         """<C> of one parameter set — the optimiser-loop call (reference
         qaoa_objective, qaoa.py:185-194, bound to this simulator): the
@@ -271,6 +300,17 @@ class QaoaSimulator:
         if initial is not None or self.mixer.kind != "x":
             res = self.simulate_qaoa(gammas, betas, initial=initial, reuse_buffer=True)
             return float(res.cached_expectation().item())
+        gctx = self._graph_ctx
+        if gctx is not None and self.use_graph and gctx[0] == len(gammas) == len(betas):
+            # small states (n <= 12): replay the captured graph of this depth -- the
+            # kernel reads the angles from this pinned array and writes the objective
+            # into pinned memory (fq_objective_graph_run)
+            og = gctx[1]
+            og.ang[0::2] = gammas
+            og.ang[1::2] = betas
+            val = og.run()
+            increment_version(self._buffer)
+            return val
         gs, bs = tuple(float(g) for g in gammas), tuple(float(b) for b in betas)
         if len(gs) != len(bs):
             raise ValueError(f"{len(gs)} gammas but {len(bs)} betas")
@@ -300,6 +340,10 @@ class QaoaSimulator:
         for i, (g, b) in enumerate(zip(gs, bs)):
             L = arr[i]
             L.gamma, L.beta, L.apply_phase, L.q_lo, L.q_hi = g, b, 1, 0, self.n
+        if self.n <= 12 and self.dtype == torch.complex128 and self.use_graph and len(gs) <= 64:
+            # first evaluation at this depth: capture the graph, then replay it (above)
+            self._graph_ctx = (len(gs), _ObjectiveGraph(desc, len(gs), self._buffer, ctx[3]))
+            return self.objective(gs, bs)
         _lib.check(fn(ctypes.byref(desc), ctypes.byref(out), _lib.stream()), "fq_qaoa_objective")
         increment_version(self._buffer)  # a reuse_buffer result's state was overwritten
         return out.value

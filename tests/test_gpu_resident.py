@@ -21,7 +21,7 @@ ATOL = 1e-10
 def res16_off():
     _lib.call("fq_set_option", b"res16", 0)
     yield
-    _lib.call("fq_set_option", b"res16", 1)
+    _lib.call("fq_set_option", b"res16", 2)  # the default (k_resident8)
 
 
 def _float_poly(n, seed):
@@ -117,3 +117,36 @@ def test_objective_fast_path(n):
         assert e == pytest.approx(O.expectation(O.simulate(costs, g, b), costs), rel=1e-10, abs=1e-12)
     with pytest.raises(ValueError, match="gammas but"):
         sim.objective([0.1, 0.2], [0.3])
+
+
+@pytest.fixture(params=[2, 1, 0], ids=["resident8", "resident16", "sweep"])
+def res_variant(request):
+    _lib.call("fq_set_option", b"res16", request.param)
+    yield request.param
+    _lib.call("fq_set_option", b"res16", 2)
+
+
+@pytest.mark.parametrize("n", [5, 12])
+@pytest.mark.parametrize("float_costs", [False, True])
+def test_objective_graph_replay(n, float_costs, res_variant):
+    """objective() for n <= 12 replays a captured CUDA graph (fq_objective_graph_*:
+    angles H2D from pinned memory, the one-CTA program reading them on the device,
+    objective D2H): equal to the eager fq_qaoa_objective path and to the oracle over
+    many angle sets (gamma = 0 layers included, both RX forms), a depth change
+    (a new graph) and uint16 / float64 diagonals."""
+    poly = _float_poly(n, 3) if float_costs else labs_terms(n)
+    sim = QaoaSimulator(terms=poly)
+    costs = sim.get_cost_diagonal()
+    rng = np.random.default_rng(40 + n)
+    for p in (4, 4, 4, 7, 4):
+        g, b = rng.uniform(-1, 1, p), rng.uniform(-1.6, 1.6, p)
+        g[rng.integers(0, p)] = 0.0
+        sim.use_graph = True
+        e_graph = sim.objective(g, b)
+        sim.use_graph = False
+        e_eager = sim.objective(g, b)
+        assert e_graph == pytest.approx(e_eager, rel=1e-13, abs=1e-14)
+        assert e_graph == pytest.approx(O.expectation(O.simulate(costs, g, b), costs), rel=1e-10, abs=1e-12)
+    sim.use_graph = True
+    assert sim._graph_ctx is not None and sim._graph_ctx[0] == 4
+    del sim  # the graph handle is released with the simulator (weakref finalizer)
