@@ -35,6 +35,7 @@
 //    in its shared-memory / FP64 rounds.
 //  * States of n <= 12 qubits run the entire program in one CTA (smem-resident),
 //    which is also the batched multi-parameter path for optimiser loops.
+#include <chrono>
 #include <string>
 
 #include "sweep.cuh"
@@ -63,6 +64,9 @@ struct ResParams {
     unsigned char gates[kResMaxGates][2];
     // per (batch row, layer) angles: gam[b*p + l], bet[b*p + l]; row b = blockIdx.x
     double gam[kResMaxLayers], bet[kResMaxLayers];
+    int all_tables;         // k_resident8 with ang: uint16 phase tables of every layer built at once
+    unsigned *done_ctr;     // graph replays: device counter, and its new value published to the pinned
+    unsigned *done_flag;    //   host flag after the objective (the host spins on it instead of a stream sync)
     const double *ang;      // non-null (one parameter set): device [2p] = gamma_l, beta_l, read instead of
                             // gam / bet -- a captured CUDA graph replays with new angles (fq_objective_graph_*)
     unsigned char phase_on[kResMaxLayers];  // indexed by layer (shared by all rows)
@@ -72,6 +76,16 @@ struct ResParams {
 // Graph-replayed objective (ResParams::ang set): the angles live in pinned host
 // memory the device reads directly; staged once per CTA in shared memory.
 constexpr int kResGraphMaxLayers = 64;
+
+// thread 0, after writing the objective: make it visible system-wide, then bump the
+// replay counter and publish its value to the pinned host flag
+__device__ __forceinline__ void res_publish(const ResParams &P) {
+    if (P.done_flag) {
+        __threadfence_system();
+        const unsigned v = atomicAdd(P.done_ctr, 1u) + 1u;
+        *reinterpret_cast<volatile unsigned *>(P.done_flag) = v;
+    }
+}
 __device__ __forceinline__ void res_stage_angles(const ResParams &P, double *s_ang) {
     if (P.ang) {
         for (int i = threadIdx.x; i < 2 * P.p; i += blockDim.x) s_ang[i] = P.ang[i];
@@ -164,7 +178,10 @@ __global__ void __launch_bounds__(kResThreads) k_resident(const __grid_constant_
             acc += c * (x.x * x.x + x.y * x.y);
         }
         const double t = block_sum<kResThreads>(acc, red);
-        if (tid == 0) P.exp_out[b] = t;
+        if (tid == 0) {
+            P.exp_out[b] = t;
+            res_publish(P);
+        }
     }
     if (P.psi_out) {
         double2 *dst = P.psi_out + (long long)b * N;
@@ -330,7 +347,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_resident16(const __grid_constan
     }
     if (P.exp_out) {
         const double t = block_sum<kThreads>(acc, red);
-        if (tid == 0) P.exp_out[b] = t;
+        if (tid == 0) {
+            P.exp_out[b] = t;
+            res_publish(P);
+        }
     }
 }
 
@@ -342,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_resident16(const __grid_constan
 constexpr int kRes8Threads = 512;
 constexpr int kRes8Regs = 8;
 constexpr int kRes8Padded = kTile + kTile / 8;
-constexpr int kRes8Smem = (kRes8Padded + (kTableLo + kMaxTableHi) * 8) * (int)sizeof(double2);
+constexpr int kRes8Smem = 224 * 1024;  // max dynamic smem (all_tables: every layer's phase tables)
 
 // register pattern k (k = 0..3): registers hold tile bits 3k..3k+2
 __device__ __forceinline__ Res16Pat res8_pat(int k, int tid) {
@@ -368,6 +388,21 @@ __global__ void __launch_bounds__(kRes8Threads, 1) k_resident8(const __grid_cons
     res_stage_angles(P, s_ang);
     const int tid = threadIdx.x, N = 1 << P.n, b = blockIdx.x;
     const int table_hi = COST == FQ_COST_U16 ? P.table_hi : 0;
+    const int rows = kTableLo + table_hi;
+    if (COST == FQ_COST_U16 && P.all_tables) {
+        // graph-replayed evaluation: the tables of all layers in one parallel sweep and one
+        // barrier (instead of one sincos round + barrier per layer on the critical path)
+        for (int i = tid; i < P.p * rows; i += kRes8Threads) {
+            const int l = i / rows, r = i - l * rows;
+            double sn, cn;
+            if (r < kTableLo) sincos(s_ang[2 * l] * (P.cost_scale * (double)r), &sn, &cn);
+            else sincos(s_ang[2 * l] * (P.cost_scale * (double)(64 * (r - kTableLo)) + P.cost_offset), &sn, &cn);
+            double2 *row = tlo + ((size_t)l * rows + r) * 8;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) row[k] = make_double2(cn, -sn);
+        }
+        __syncthreads();
+    }
     double2 v[kRes8Regs];
     int pat = 3;
     Res16Pat cur = res8_pat(pat, tid);
@@ -381,7 +416,11 @@ __global__ void __launch_bounds__(kRes8Threads, 1) k_resident8(const __grid_cons
     for (int l = 0; l < P.p; ++l) {
         const double gamma = P.ang ? s_ang[2 * l] : P.gam[b * P.p + l];
         if (P.phase_on[l] && gamma != 0.0) {
-            if (COST == FQ_COST_U16 && table_hi > 0) {
+            const double2 *tl = tlo, *th = thi;
+            if (COST == FQ_COST_U16 && P.all_tables) {
+                tl = tlo + (size_t)l * rows * 8;
+                th = tl + kTableLo * 8;
+            } else if (COST == FQ_COST_U16 && table_hi > 0) {
                 build_phase_tables<double>(tlo, thi, table_hi, gamma, P.cost_scale, P.cost_offset);
                 __syncthreads();
             }
@@ -392,7 +431,7 @@ __global__ void __launch_bounds__(kRes8Threads, 1) k_resident8(const __grid_cons
                 double2 f;
                 if (COST == FQ_COST_U16 && table_hi > 0) {
                     const unsigned raw = static_cast<const uint16_t *>(P.costs)[e];
-                    f = cmul(thi[(raw >> 6) * 8 + (tid & 7)], tlo[(raw & 63) * 8 + (tid & 7)]);
+                    f = cmul(th[(raw >> 6) * 8 + (tid & 7)], tl[(raw & 63) * 8 + (tid & 7)]);
                 } else {
                     f = res16_phase_sincos<COST>(P, e, gamma);
                 }
@@ -469,7 +508,10 @@ __global__ void __launch_bounds__(kRes8Threads, 1) k_resident8(const __grid_cons
     }
     if (P.exp_out) {
         const double t = block_sum<kRes8Threads>(acc, red);
-        if (tid == 0) P.exp_out[b] = t;
+        if (tid == 0) {
+            P.exp_out[b] = t;
+            res_publish(P);
+        }
     }
     (void)pat;
 }
@@ -1371,7 +1413,7 @@ static int launch_resident(const ResParams &P, int batch, const double *su2_dev,
             configured8 = true;
         }
         const int th = COST == FQ_COST_U16 ? P.table_hi : 0;
-        const size_t smem8 = (size_t)(kRes8Padded + (kTableLo + th) * 8) * sizeof(double2);
+        const size_t smem8 = (size_t)(kRes8Padded + (P.all_tables ? P.p : 1) * (kTableLo + th) * 8) * sizeof(double2);
         if (P.mixer == FQ_MIXER_X) k_resident8<COST, MIX_RX><<<batch, kRes8Threads, smem8, st>>>(P, su2_dev);
         else k_resident8<COST, MIX_SU2><<<batch, kRes8Threads, smem8, st>>>(P, su2_dev);
         FQ_LAUNCHED("k_resident8");
@@ -1485,6 +1527,9 @@ struct ObjGraph {
     cudaGraphExec_t exec = nullptr;
     cudaStream_t st = nullptr;
     cudaEvent_t ev = nullptr;
+    unsigned *ctr = nullptr;              // device replay counter
+    volatile unsigned *flag = nullptr;    // pinned host flag the kernel publishes the counter to
+    unsigned expected = 0;
 };
 
 static void obj_graph_free(ObjGraph *g) {
@@ -1493,6 +1538,8 @@ static void obj_graph_free(ObjGraph *g) {
     if (g->graph) cudaGraphDestroy(g->graph);
     if (g->ev) cudaEventDestroy(g->ev);
     if (g->st) cudaStreamDestroy(g->st);
+    if (g->ctr) cudaFree(g->ctr);
+    if (g->flag) cudaFreeHost(const_cast<unsigned *>(g->flag));
     delete g;
 }
 
@@ -1527,6 +1574,15 @@ int fq_objective_graph_create(const fq_evolve_desc *d, const double *ang_host, d
         return fail(e, "cudaHostGetDevicePointer(objective): out_host must be pinned");
     if ((e = cudaStreamCreateWithFlags(&g->st, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "cudaStreamCreate");
     if ((e = cudaEventCreateWithFlags(&g->ev, cudaEventDisableTiming)) != cudaSuccess) return fail(e, "cudaEventCreate");
+    if ((e = cudaMalloc(&g->ctr, sizeof(unsigned))) != cudaSuccess) return fail(e, "cudaMalloc(counter)");
+    if ((e = cudaMemset(g->ctr, 0, sizeof(unsigned))) != cudaSuccess) return fail(e, "cudaMemset(counter)");
+    unsigned *flag_host = nullptr, *flag_dev = nullptr;
+    if ((e = cudaHostAlloc(reinterpret_cast<void **>(&flag_host), sizeof(unsigned), cudaHostAllocMapped)) != cudaSuccess)
+        return fail(e, "cudaHostAlloc(flag)");
+    *flag_host = 0;
+    g->flag = flag_host;
+    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&flag_dev), flag_host, 0)) != cudaSuccess)
+        return fail(e, "cudaHostGetDevicePointer(flag)");
     ResParams *P = new ResParams;
     std::memset(P, 0, sizeof *P);
     P->n = d->n;
@@ -1537,10 +1593,16 @@ int fq_objective_graph_create(const fq_evolve_desc *d, const double *ang_host, d
     P->cost_offset = d->cost_offset;
     P->init = 1;
     P->init_amp = d->init_amp;
-    P->psi_out = static_cast<double2 *>(d->psi);
+    P->psi_out = nullptr;  // the objective only: the final state is not written back
     P->exp_out = out_dev;
     P->table_hi = d->cost_kind == FQ_COST_U16 && g_phase_tables ? table_rows(d->cost_levels) : 0;
     P->ang = ang_dev;
+    P->done_ctr = g->ctr;
+    P->done_flag = flag_dev;
+    // every layer's uint16 phase tables at kernel start, when they fit the shared memory
+    P->all_tables = (d->cost_kind == FQ_COST_U16 && P->table_hi > 0 && g_res16 == 2 &&
+                     (size_t)(kRes8Padded + (size_t)p * (kTableLo + P->table_hi) * 8) * sizeof(double2) <=
+                         (size_t)kRes8Smem) ? 1 : 0;
     for (int i = 0; i < p; ++i) {
         P->phase_on[i] = (unsigned char)(d->layers[i].apply_phase != 0);
         P->qlo[i] = (unsigned char)std::max(0, std::min(d->n, d->layers[i].q_lo));
@@ -1564,6 +1626,7 @@ int fq_objective_graph_create(const fq_evolve_desc *d, const double *ang_host, d
         s = s2 ? s2 : (e != cudaSuccess ? cuda_status(e, "cudaStreamEndCapture") : FQ_OK);
     }
     if (!s && (e = cudaGraphInstantiate(&g->exec, g->graph, 0)) != cudaSuccess) s = cuda_status(e, "cudaGraphInstantiate");
+    g->expected = *g->flag;  // the eager run's publication
     delete P;
     if (s) {
         obj_graph_free(g);
@@ -1576,10 +1639,24 @@ int fq_objective_graph_create(const fq_evolve_desc *d, const double *ang_host, d
 int fq_objective_graph_run(void *handle, void *stream) {
     FQ_CHECK_ARG(handle, "fq_objective_graph_run: null handle");
     ObjGraph *g = static_cast<ObjGraph *>(handle);
-    // on the caller's stream (ordered behind its work), then wait for it
+    // on the caller's stream (ordered behind its work); completion is detected by
+    // spinning on the pinned flag the kernel publishes after the objective (a
+    // stream synchronisation's wake-up costs several microseconds); after 2 s of
+    // spinning, the stream is synchronised to surface an error instead
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     FQ_CUDA(cudaGraphLaunch(g->exec, st));
-    FQ_CUDA(cudaStreamSynchronize(st));
+    const unsigned want = ++g->expected;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned spins = 0; *g->flag != want; ++spins) {
+        if ((spins & 1023) == 1023 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
+            FQ_CUDA(cudaStreamSynchronize(st));
+            if (*g->flag != want) {
+                set_error("fq_objective_graph_run: the evaluation did not publish its objective");
+                return FQ_ERR_UNSUPPORTED;
+            }
+            break;
+        }
+    }
     return FQ_OK;
 }
 
