@@ -217,9 +217,11 @@ int fq_qaoa_objective(const fq_evolve_desc *desc, double *out_host, void *stream
  * BASELINE config 1): create() captures the one-CTA resident program once per
  * descriptor, reading the angles ang_host[2p] = (gamma_l, beta_l) from and
  * writing the objective to *out_host -- both PINNED host buffers, accessed by
- * the kernel directly (no copies); run() orders it behind `stream`, launches
- * the graph and synchronises, after the caller wrote new angles into ang_host.
- * desc's device buffers (state, costs) must outlive the handle. */
+ * the kernel directly (no copies); run() launches the graph on `stream` (after
+ * the caller wrote new angles into ang_host) and returns once the kernel has
+ * published the objective (it spins on a pinned completion flag; the stream
+ * may still be retiring the kernel).  desc's device buffers (state, costs)
+ * must outlive the handle; the final state is not written back. */
 int fq_objective_graph_create(const fq_evolve_desc *desc, const double *ang_host, double *out_host, void **handle);
 int fq_objective_graph_run(void *handle, void *stream);
 int fq_objective_graph_destroy(void *handle);
