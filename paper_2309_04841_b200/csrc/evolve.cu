@@ -65,8 +65,6 @@ struct ResParams {
     // per (batch row, layer) angles: gam[b*p + l], bet[b*p + l]; row b = blockIdx.x
     double gam[kResMaxLayers], bet[kResMaxLayers];
     int all_tables;         // k_resident8 with ang: uint16 phase tables of every layer built at once
-    unsigned *done_ctr;     // graph replays: device counter, and its new value published to the pinned
-    unsigned *done_flag;    //   host flag after the objective (the host spins on it instead of a stream sync)
     const double *ang;      // non-null (one parameter set): device [2p] = gamma_l, beta_l, read instead of
                             // gam / bet -- a captured CUDA graph replays with new angles (fq_objective_graph_*)
     unsigned char phase_on[kResMaxLayers];  // indexed by layer (shared by all rows)
@@ -77,15 +75,6 @@ struct ResParams {
 // memory the device reads directly; staged once per CTA in shared memory.
 constexpr int kResGraphMaxLayers = 64;
 
-// thread 0, after writing the objective: make it visible system-wide, then bump the
-// replay counter and publish its value to the pinned host flag
-__device__ __forceinline__ void res_publish(const ResParams &P) {
-    if (P.done_flag) {
-        __threadfence_system();
-        const unsigned v = atomicAdd(P.done_ctr, 1u) + 1u;
-        *reinterpret_cast<volatile unsigned *>(P.done_flag) = v;
-    }
-}
 __device__ __forceinline__ void res_stage_angles(const ResParams &P, double *s_ang) {
     if (P.ang) {
         for (int i = threadIdx.x; i < 2 * P.p; i += blockDim.x) s_ang[i] = P.ang[i];
@@ -178,10 +167,7 @@ __global__ void __launch_bounds__(kResThreads) k_resident(const __grid_constant_
             acc += c * (x.x * x.x + x.y * x.y);
         }
         const double t = block_sum<kResThreads>(acc, red);
-        if (tid == 0) {
-            P.exp_out[b] = t;
-            res_publish(P);
-        }
+        if (tid == 0) P.exp_out[b] = t;
     }
     if (P.psi_out) {
         double2 *dst = P.psi_out + (long long)b * N;
@@ -347,10 +333,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_resident16(const __grid_constan
     }
     if (P.exp_out) {
         const double t = block_sum<kThreads>(acc, red);
-        if (tid == 0) {
-            P.exp_out[b] = t;
-            res_publish(P);
-        }
+        if (tid == 0) P.exp_out[b] = t;
     }
 }
 
@@ -508,10 +491,7 @@ __global__ void __launch_bounds__(kRes8Threads, 1) k_resident8(const __grid_cons
     }
     if (P.exp_out) {
         const double t = block_sum<kRes8Threads>(acc, red);
-        if (tid == 0) {
-            P.exp_out[b] = t;
-            res_publish(P);
-        }
+        if (tid == 0) P.exp_out[b] = t;
     }
     (void)pat;
 }
@@ -1527,10 +1507,12 @@ struct ObjGraph {
     cudaGraphExec_t exec = nullptr;
     cudaStream_t st = nullptr;
     cudaEvent_t ev = nullptr;
-    unsigned *ctr = nullptr;              // device replay counter
-    volatile unsigned *flag = nullptr;    // pinned host flag the kernel publishes the counter to
-    unsigned expected = 0;
+    volatile unsigned long long *out = nullptr;  // the pinned objective slot (bit pattern)
 };
+
+// Written into the objective slot before each replay; the kernel's 8-byte store of
+// the objective replaces it (a NaN payload no arithmetic produces).
+constexpr unsigned long long kObjPending = 0x7ff4dead00c0ffeeULL;
 
 static void obj_graph_free(ObjGraph *g) {
     if (!g) return;
@@ -1538,8 +1520,6 @@ static void obj_graph_free(ObjGraph *g) {
     if (g->graph) cudaGraphDestroy(g->graph);
     if (g->ev) cudaEventDestroy(g->ev);
     if (g->st) cudaStreamDestroy(g->st);
-    if (g->ctr) cudaFree(g->ctr);
-    if (g->flag) cudaFreeHost(const_cast<unsigned *>(g->flag));
     delete g;
 }
 
@@ -1574,15 +1554,7 @@ int fq_objective_graph_create(const fq_evolve_desc *d, const double *ang_host, d
         return fail(e, "cudaHostGetDevicePointer(objective): out_host must be pinned");
     if ((e = cudaStreamCreateWithFlags(&g->st, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "cudaStreamCreate");
     if ((e = cudaEventCreateWithFlags(&g->ev, cudaEventDisableTiming)) != cudaSuccess) return fail(e, "cudaEventCreate");
-    if ((e = cudaMalloc(&g->ctr, sizeof(unsigned))) != cudaSuccess) return fail(e, "cudaMalloc(counter)");
-    if ((e = cudaMemset(g->ctr, 0, sizeof(unsigned))) != cudaSuccess) return fail(e, "cudaMemset(counter)");
-    unsigned *flag_host = nullptr, *flag_dev = nullptr;
-    if ((e = cudaHostAlloc(reinterpret_cast<void **>(&flag_host), sizeof(unsigned), cudaHostAllocMapped)) != cudaSuccess)
-        return fail(e, "cudaHostAlloc(flag)");
-    *flag_host = 0;
-    g->flag = flag_host;
-    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&flag_dev), flag_host, 0)) != cudaSuccess)
-        return fail(e, "cudaHostGetDevicePointer(flag)");
+    g->out = reinterpret_cast<volatile unsigned long long *>(out_host);
     ResParams *P = new ResParams;
     std::memset(P, 0, sizeof *P);
     P->n = d->n;
@@ -1597,8 +1569,6 @@ int fq_objective_graph_create(const fq_evolve_desc *d, const double *ang_host, d
     P->exp_out = out_dev;
     P->table_hi = d->cost_kind == FQ_COST_U16 && g_phase_tables ? table_rows(d->cost_levels) : 0;
     P->ang = ang_dev;
-    P->done_ctr = g->ctr;
-    P->done_flag = flag_dev;
     // every layer's uint16 phase tables at kernel start, when they fit the shared memory
     P->all_tables = (d->cost_kind == FQ_COST_U16 && P->table_hi > 0 && g_res16 == 2 &&
                      (size_t)(kRes8Padded + (size_t)p * (kTableLo + P->table_hi) * 8) * sizeof(double2) <=
@@ -1626,7 +1596,6 @@ int fq_objective_graph_create(const fq_evolve_desc *d, const double *ang_host, d
         s = s2 ? s2 : (e != cudaSuccess ? cuda_status(e, "cudaStreamEndCapture") : FQ_OK);
     }
     if (!s && (e = cudaGraphInstantiate(&g->exec, g->graph, 0)) != cudaSuccess) s = cuda_status(e, "cudaGraphInstantiate");
-    g->expected = *g->flag;  // the eager run's publication
     delete P;
     if (s) {
         obj_graph_free(g);
@@ -1640,18 +1609,19 @@ int fq_objective_graph_run(void *handle, void *stream) {
     FQ_CHECK_ARG(handle, "fq_objective_graph_run: null handle");
     ObjGraph *g = static_cast<ObjGraph *>(handle);
     // on the caller's stream (ordered behind its work); completion is detected by
-    // spinning on the pinned flag the kernel publishes after the objective (a
-    // stream synchronisation's wake-up costs several microseconds); after 2 s of
-    // spinning, the stream is synchronised to surface an error instead
+    // spinning on the pinned objective slot until the kernel's 8-byte store replaces
+    // the pending pattern (a stream synchronisation's wake-up costs several
+    // microseconds); after 2 s of spinning, the stream is synchronised to surface
+    // an error instead
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    *g->out = kObjPending;
     FQ_CUDA(cudaGraphLaunch(g->exec, st));
-    const unsigned want = ++g->expected;
     const auto t0 = std::chrono::steady_clock::now();
-    for (unsigned spins = 0; *g->flag != want; ++spins) {
+    for (unsigned spins = 0; *g->out == kObjPending; ++spins) {
         if ((spins & 1023) == 1023 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
             FQ_CUDA(cudaStreamSynchronize(st));
-            if (*g->flag != want) {
-                set_error("fq_objective_graph_run: the evaluation did not publish its objective");
+            if (*g->out == kObjPending) {
+                set_error("fq_objective_graph_run: the evaluation did not write its objective");
                 return FQ_ERR_UNSUPPORTED;
             }
             break;
